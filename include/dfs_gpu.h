@@ -1,0 +1,215 @@
+/* include/dfs_gpu.h — the drop-in C ABI of the B200-native DFSAttn hot path.
+ *
+ * Plain C: POD arguments, raw device pointers, sizes and a cudaStream_t passed
+ * as void*. No torch / C++ types cross this boundary. The C++ drop-in shim
+ * (include/dfs/*.hpp, namespace dfs::) is implemented on top of these entry
+ * points; Python (paper_2605_23445_b200/_capi.py) binds them with ctypes.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   reorder      include/dfs/curve.hpp:28-54        (curve.cpp:27-185)
+ *   score/mask   include/dfs/mask_builder.hpp:27-57 (mask_builder.cpp:12-124)
+ *   sparse-attn  include/dfs/attention.hpp:20-33    (attention.cpp:95-159)
+ *   mask cache   include/dfs/scheduler.hpp:20-140   (scheduler.cpp:18-186)
+ *
+ * Conventions
+ *   - Status: 0 ok; negative on error. DFS_E_INVALID mirrors the reference's
+ *     std::invalid_argument, DFS_E_RANGE its std::out_of_range. The message is
+ *     thread-local: dfs_last_error().
+ *   - Every entry point is reentrant; a dfs_handle owns workspaces and the
+ *     device mask cache and must not be used by two threads at once (one
+ *     handle per thread or per stream). Nothing else is global.
+ *   - Token tensors on device are either
+ *       NHD: [N, H, d] token-major (raster order; the caller's activations), or
+ *       HND: [H, N, d] head-major (reordered; the path's internal layout).
+ *     dtype is DFS_BF16 (performance path) or DFS_F32 (drop-in Matrix path).
+ *   - Block masks are CSR over (head, query block): blk_ptr[H*M+1] and
+ *     blk_idx[nnz] ascending key-block indices, or BlockMask bit payloads
+ *     (M*M bits row-major, MSB-first, block_mask.hpp:15-80).
+ *   - No CPU fallback: unsupported geometry returns DFS_E_UNSUPPORTED.
+ */
+#ifndef DFS_GPU_H
+#define DFS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFS_ABI_VERSION 1
+
+enum dfs_status {
+  DFS_OK = 0,
+  DFS_E_INVALID = -1,     /* std::invalid_argument in the reference */
+  DFS_E_RANGE = -2,       /* std::out_of_range in the reference */
+  DFS_E_UNSUPPORTED = -3, /* geometry outside the compiled kernels' contract */
+  DFS_E_CUDA = -4,        /* CUDA runtime / launch failure */
+  DFS_E_INTERNAL = -5
+};
+
+enum dfs_dtype { DFS_BF16 = 0, DFS_F32 = 1 };
+enum dfs_layout { DFS_NHD = 0, DFS_HND = 1 };
+/* curve.hpp:12 Ordering, same numeric values as the enum's declaration order */
+enum dfs_ordering { DFS_RASTER = 0, DFS_HILBERT2D = 1, DFS_BLOCK3D = 2, DFS_HILBERT3D = 3 };
+
+typedef struct dfs_handle dfs_handle;
+typedef void* dfs_stream; /* cudaStream_t */
+
+const char* dfs_last_error(void);
+int dfs_abi_version(void);
+
+/* ---- handle: workspaces + per-geometry permutation cache + mask cache ---- */
+int dfs_handle_create(dfs_handle** out, int device);
+int dfs_handle_destroy(dfs_handle* h);
+
+/* ======================= K1: token ordering (curve.hpp) =================== */
+/* curve.hpp:31-48 order_tokens / hilbert3d_order / ...: forward[i] = raster
+ * index of the token at reordered position i. inv may be NULL; when given,
+ * inv[forward[i]] = i (curve.hpp:53 invert_permutation). Device outputs. */
+int dfs_order_tokens(int ordering, int64_t frames, int64_t height, int64_t width, uint32_t* fwd,
+                     uint32_t* inv, dfs_stream stream);
+/* curve.hpp:53 invert_permutation on device. */
+int dfs_invert_permutation(const uint32_t* fwd, int64_t n, uint32_t* inv, dfs_stream stream);
+/* curve.hpp:27 validate_permutation: *ok_host = 1 iff fwd is a bijection on [0,n).
+ * Synchronises the stream. */
+int dfs_validate_permutation(dfs_handle* h, const uint32_t* fwd, int64_t n, int* ok_host,
+                             dfs_stream stream);
+
+/* ================ K2/K6: permute / unpermute (curve.hpp:50,53) ============== */
+/* dst row i <- src row idx[i] for every head (curve.cpp:166 apply_permutation),
+ * converting layout src_layout -> dst_layout. With pooled != NULL also emits
+ * the sub-block means of the DESTINATION rows (mask_builder.cpp:12 mean_pool,
+ * zero-padded last group divided by pool) as fp32 [H, ceil(n/pool), d].
+ * With nonfinite != NULL atomically ORs 1 into *nonfinite when any element is
+ * NaN/Inf (attention.cpp:19-20 check). */
+int dfs_permute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype,
+                     const uint32_t* idx, int64_t n, int64_t heads, int64_t d, float* pooled,
+                     int64_t pool, int32_t* nonfinite, dfs_stream stream);
+/* Inverse direction: dst row idx[i] <- src row i (scatter), i.e.
+ * apply_permutation(invert_permutation(p), x) without materialising inv. */
+int dfs_unpermute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype,
+                       const uint32_t* idx, int64_t n, int64_t heads, int64_t d,
+                       dfs_stream stream);
+
+/* ================= K3/K4: hierarchical scoring + selection ================ */
+/* mask_builder.cpp:30-80,115-117 block_scores from POOLED inputs:
+ * pq [H, M*subs, d] fp32 (zero rows past ceil(n/Bs)), pk [H, ceil(n/Bs), d]
+ * fp32; S [H, M, M] fp64, rows sum to subs. fp32-accurate tensor-core GEMM +
+ * fp32 softmax with fp64 tile sums. */
+int dfs_score_blocks(dfs_handle* h, const float* pq, const float* pk, int64_t heads, int64_t n,
+                     int64_t d, int64_t block, int64_t sub_block, double* scores,
+                     dfs_stream stream);
+/* mask_builder.cpp:82-87 topk_count (host). */
+int dfs_topk_count(double budget, int64_t m, int64_t* k);
+/* mask_builder.cpp:91-113 topk_select on device, per (head, row): the K best
+ * key blocks under (score desc, index asc), ascending. scores [H, M, M] fp64;
+ * lut [H, M, K] int32 (may be NULL); bits [H, ceil(M*M/8)] BlockMask payloads
+ * (may be NULL; zeroed by the call). Bit-exact with the reference given the
+ * same scores. */
+int dfs_topk_select(const double* scores, int64_t heads, int64_t m, int64_t k, int32_t* lut,
+                    uint8_t* bits, dfs_stream stream);
+/* BlockMask payloads [H][ceil(M*M/8)] -> CSR (blk_ptr [H*M+1], blk_idx cap
+ * H*M*M). Returns DFS_E_INVALID (after a stream sync) if a row is empty
+ * (attention.cpp:133-136). nnz_host may be NULL. */
+int dfs_mask_bits_to_csr(dfs_handle* h, const uint8_t* bits, int64_t heads, int64_t m,
+                         int32_t* blk_ptr, int32_t* blk_idx, int64_t* nnz_host,
+                         dfs_stream stream);
+/* Uniform-K LUT [H, M, K] -> CSR row pointers blk_ptr [H*M+1] (blk_idx = lut). */
+int dfs_lut_row_ptr(int64_t heads, int64_t m, int64_t k, int32_t* blk_ptr, dfs_stream stream);
+
+/* ===================== K5: block-sparse attention forward ================= */
+/* attention.cpp:125-159 block_sparse_attention (and :95-103
+ * full_attention_output with a full mask, nq != nk allowed). Per head h and
+ * query block u the keys are the union of blocks blk_idx[blk_ptr[h*M+u] ..
+ * blk_ptr[h*M+u+1]) clipped to nk (padded keys excluded); query rows >= nq are
+ * not produced. q [.., nq, ..], k/v [.., nk, ..] in `in_layout`; o in
+ * `out_layout`. When out_rows != NULL, output row i is written to row
+ * out_rows[i] (fused unpermute: pass the forward permutation).
+ * scale <= 0 means 1/sqrt(d). fp32 softmax and accumulation. */
+typedef struct {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  int dtype;      /* DFS_BF16 | DFS_F32 (f32 uses the generic kernel) */
+  int in_layout;  /* DFS_HND | DFS_NHD */
+  int out_layout; /* DFS_HND | DFS_NHD */
+  int64_t heads;
+  int64_t nq;
+  int64_t nk;
+  int64_t d;
+  int64_t block; /* B, query and key block size */
+  const int32_t* blk_ptr;
+  const int32_t* blk_idx;
+  const uint32_t* out_rows;
+  float scale;
+  int force_generic; /* 1: use the SIMT kernel even when the tcgen05 one applies */
+} dfs_attn_args;
+int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream);
+
+/* ======================= K7: mask cache + Alg.1 step ====================== */
+/* scheduler.hpp:20-50 SparsitySchedule (host, identical rules). */
+typedef struct {
+  int total_steps;
+  double warmup_fraction;
+  const double* phase_budgets;
+  int n_budgets;
+  double phase_fraction;
+  int update_interval;
+} dfs_schedule;
+/* budget_at: *budget = -1 for a dense step; DFS_E_RANGE outside [0,T). */
+int dfs_schedule_budget_at(const dfs_schedule* s, int step, double* budget);
+int dfs_schedule_is_update_step(const dfs_schedule* s, int step, int* is_update);
+int dfs_schedule_info(const dfs_schedule* s, int* warmup_steps, int* phase_length);
+
+/* scheduler.hpp:54-71 MaskCache, device resident, owned by the handle, keyed
+ * by (layer, head). */
+int dfs_mask_cache_clear(dfs_handle* h);
+int dfs_mask_cache_contains(dfs_handle* h, int layer, int head, int* found);
+/* Copies the cached mask of (layer, head) out as a BlockMask payload (device
+ * pointer, ceil(M*M/8) bytes) and reports its last update step / block count. */
+int dfs_mask_cache_get(dfs_handle* h, int layer, int head, uint8_t* bits, int* last_update_step,
+                       int64_t* m, dfs_stream stream);
+/* Stores a BlockMask payload (device pointer) for (layer, head) at `step`. */
+int dfs_mask_cache_store(dfs_handle* h, int layer, int head, const uint8_t* bits, int64_t m,
+                         int64_t block, int step, dfs_stream stream);
+int dfs_mask_cache_size(dfs_handle* h, int64_t* n);
+
+/* scheduler.cpp:91-135 run_step for ALL heads of one layer at once.
+ * q, k, v, o: [N, H, d] bf16 raster-order activations (the DiT layout).
+ * Dense steps (warmup or force_dense) run full attention in raster order;
+ * sparse steps reorder (forward permutation `perm`, device u32[N]), build or
+ * reuse the cached (layer, head) masks, attend, and scatter back to raster
+ * order. Per-head stats go to the host arrays when non-NULL. */
+typedef struct {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  int64_t n;
+  int64_t heads;
+  int64_t d;
+  const uint32_t* perm; /* device forward permutation; NULL = hilbert3d of dims */
+  int64_t frames, height, width;
+  int64_t block;
+  int64_t sub_block;
+  int layer;
+  int step;
+  int force_dense;
+  int32_t* nonfinite;    /* optional device flag */
+  /* outputs (host, optional) */
+  int* dense_out;        /* 1 if the step ran dense */
+  double* budget_out;    /* budget (1.0 when dense) */
+  int* updated_out;      /* [H] mask_updated per head */
+  double* sparsity_out;  /* [H] realized sparsity per head (metrics.cpp:39) */
+} dfs_step_args;
+int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
+
+/* Device mem introspection for the bench (bytes of workspace held). */
+int dfs_handle_workspace_bytes(dfs_handle* h, int64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFS_GPU_H */

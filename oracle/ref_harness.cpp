@@ -336,63 +336,80 @@ int dfsref_run_trajectory(int ordering, int64_t f, int64_t h, int64_t w, int64_t
 // Per head the harness also runs the full-N reorder (hilbert3d_order,
 // apply_permutation x3) and the inverse permute once. Q/K/V are iid normal
 // (content does not change the reference's op count).
-// Returns the wall seconds of the timed region and the number of units done.
-int dfsref_sample_call(int64_t f, int64_t h, int64_t w, int64_t d, int64_t b, int64_t bs,
-                       double budget, int heads, int units_per_head, int threads,
-                       double* seconds, int64_t* units_done) {
+// dfsref_sample_prepare / _run / _free below implement it.
+struct SampleCtx {
+  GridDims dims;
+  int64_t n = 0, d = 0, b = 0, bs = 0, m = 0, kk = 0, subs = 0;
+  std::vector<Matrix> qs, ks, vs;
+};
+
+// Inputs for `heads` heads (iid normal, per-head seeds), generated in parallel.
+void* dfsref_sample_prepare(int64_t f, int64_t h, int64_t w, int64_t d, int64_t b, int64_t bs, double budget,
+                            int heads, int threads) {
+  auto* c = new SampleCtx;
+  c->dims = GridDims{f, h, w};
+  c->n = c->dims.token_count();
+  c->d = d;
+  c->b = b;
+  c->bs = bs;
+  c->m = block_count_for(c->n, b);
+  c->kk = topk_count(budget, c->m);
+  c->subs = b / bs;
+  c->qs.resize(static_cast<size_t>(heads));
+  c->ks.resize(static_cast<size_t>(heads));
+  c->vs.resize(static_cast<size_t>(heads));
+  parallel_for(heads, threads, [&](int64_t hh) {
+    RandomStream s(derive_seed(7, {static_cast<uint64_t>(hh)}));
+    Matrix q(c->n, d), k(c->n, d), v(c->n, d);
+    for (float& x : q.values()) x = static_cast<float>(s.next_gaussian());
+    for (float& x : k.values()) x = static_cast<float>(s.next_gaussian());
+    for (float& x : v.values()) x = static_cast<float>(s.next_gaussian());
+    c->qs[static_cast<size_t>(hh)] = std::move(q);
+    c->ks[static_cast<size_t>(hh)] = std::move(k);
+    c->vs[static_cast<size_t>(hh)] = std::move(v);
+  });
+  return c;
+}
+
+void dfsref_sample_free(void* ctx) { delete static_cast<SampleCtx*>(ctx); }
+
+// One timed sample: per head the full reorder + pooled keys, then
+// `units_per_head` query blocks through scoring + selection + attention.
+int dfsref_sample_run(void* ctx, int units_per_head, int threads, double* seconds) {
   return guarded([&] {
-    const GridDims dims{f, h, w};
-    const int64_t n = dims.token_count();
-    const int64_t m = block_count_for(n, b);
-    const int64_t kk = topk_count(budget, m);
-    const int64_t subs = b / bs;
-    std::vector<Matrix> qs, ks, vs;
-    for (int hh = 0; hh < heads; ++hh) {
-      RandomStream s(derive_seed(7, {static_cast<uint64_t>(hh)}));
-      Matrix q(n, d), k(n, d), v(n, d);
-      for (float& x : q.values()) x = static_cast<float>(s.next_gaussian());
-      for (float& x : k.values()) x = static_cast<float>(s.next_gaussian());
-      for (float& x : v.values()) x = static_cast<float>(s.next_gaussian());
-      qs.push_back(std::move(q));
-      ks.push_back(std::move(k));
-      vs.push_back(std::move(v));
-    }
+    SampleCtx& c = *static_cast<SampleCtx*>(ctx);
+    const int heads = static_cast<int>(c.qs.size());
+    const int64_t n = c.n, d = c.d, b = c.b, bs = c.bs, m = c.m, kk = c.kk, subs = c.subs;
     const auto t0 = std::chrono::steady_clock::now();
     // per head, once: reorder + inverse (curve.cpp:95,166,178) and the pooled
     // keys every unit of the head scores against (mask_builder.cpp:12)
     std::vector<Matrix> pks(static_cast<size_t>(heads));
     parallel_for(heads, threads, [&](int64_t hh) {
-      const Permutation p = hilbert3d_order(dims);
-      const Matrix& v = vs[static_cast<size_t>(hh)];
-      const Matrix rq = apply_permutation(p, qs[static_cast<size_t>(hh)]);
-      const Matrix rk = apply_permutation(p, ks[static_cast<size_t>(hh)]);
-      const Matrix rv = apply_permutation(p, v);
+      const Permutation p = hilbert3d_order(c.dims);
+      const Matrix rq = apply_permutation(p, c.qs[static_cast<size_t>(hh)]);
+      const Matrix rk = apply_permutation(p, c.ks[static_cast<size_t>(hh)]);
+      const Matrix rv = apply_permutation(p, c.vs[static_cast<size_t>(hh)]);
       (void)apply_permutation(invert_permutation(p), rv);
-      pks[static_cast<size_t>(hh)] = mean_pool(ks[static_cast<size_t>(hh)], bs);
+      pks[static_cast<size_t>(hh)] = mean_pool(c.ks[static_cast<size_t>(hh)], bs);
     });
     parallel_for(static_cast<int64_t>(heads) * units_per_head, threads, [&](int64_t item) {
       const int hh = static_cast<int>(item / units_per_head);
       const int64_t slot = item % units_per_head;
-      // spread the sampled units over the head
-      const int64_t u = (slot * m) / units_per_head;
-      const Matrix& q = qs[static_cast<size_t>(hh)];
-      const Matrix& k = ks[static_cast<size_t>(hh)];
-      const Matrix& v = vs[static_cast<size_t>(hh)];
+      const int64_t u = (slot * m) / units_per_head;  // spread the sampled units over the head
+      const Matrix& q = c.qs[static_cast<size_t>(hh)];
+      const Matrix& k = c.ks[static_cast<size_t>(hh)];
+      const Matrix& v = c.vs[static_cast<size_t>(hh)];
       const Matrix& pk = pks[static_cast<size_t>(hh)];
-      // scoring for block u (mask_builder.cpp:12,30,64; attention.cpp:105):
-      // the unit's pooled query rows, zero rows past the end (mask_builder.cpp:40-49)
+      // scoring for block u (mask_builder.cpp:12,30,64; attention.cpp:105): the
+      // unit's pooled query rows, zero rows past the end (mask_builder.cpp:40-49)
       const int64_t qlo = u * b, qhi = std::min(qlo + b, n);
-      const Matrix pq_part = mean_pool(
-          [&] {
-            Matrix x(qhi - qlo, d);
-            for (int64_t i = qlo; i < qhi; ++i)
-              for (int64_t c = 0; c < d; ++c) x.at(i - qlo, c) = q.at(i, c);
-            return x;
-          }(),
-          bs);
+      Matrix xq(qhi - qlo, d);
+      for (int64_t i = qlo; i < qhi; ++i)
+        for (int64_t cc = 0; cc < d; ++cc) xq.at(i - qlo, cc) = q.at(i, cc);
+      const Matrix pq_part = mean_pool(xq, bs);
       Matrix pq(subs, d);
       for (int64_t r = 0; r < pq_part.rows(); ++r)
-        for (int64_t c = 0; c < d; ++c) pq.at(r, c) = pq_part.at(r, c);
+        for (int64_t cc = 0; cc < d; ++cc) pq.at(r, cc) = pq_part.at(r, cc);
       const Matrix sc = attention_scores(pq, pk);
       std::vector<double> row(static_cast<size_t>(m), 0.0);
       for (int64_t r = 0; r < subs; ++r)
@@ -402,21 +419,16 @@ int dfsref_sample_call(int64_t f, int64_t h, int64_t w, int64_t d, int64_t b, in
       std::vector<int64_t> keys;
       for (int32_t vb : sel)
         for (int64_t j = vb * b; j < std::min((vb + 1) * b, n); ++j) keys.push_back(j);
-      const int64_t lo = u * b, hi = std::min(lo + b, n);
-      Matrix qu(hi - lo, d), ksel(static_cast<int64_t>(keys.size()), d),
-          vsel(static_cast<int64_t>(keys.size()), d);
-      for (int64_t i = lo; i < hi; ++i)
-        for (int64_t c = 0; c < d; ++c) qu.at(i - lo, c) = q.at(i, c);
+      Matrix ksel(static_cast<int64_t>(keys.size()), d), vsel(static_cast<int64_t>(keys.size()), d);
       for (size_t j = 0; j < keys.size(); ++j)
-        for (int64_t c = 0; c < d; ++c) {
-          ksel.at(static_cast<int64_t>(j), c) = k.at(keys[j], c);
-          vsel.at(static_cast<int64_t>(j), c) = v.at(keys[j], c);
+        for (int64_t cc = 0; cc < d; ++cc) {
+          ksel.at(static_cast<int64_t>(j), cc) = k.at(keys[j], cc);
+          vsel.at(static_cast<int64_t>(j), cc) = v.at(keys[j], cc);
         }
-      (void)full_attention_output(qu, ksel, vsel);
+      (void)full_attention_output(xq, ksel, vsel);
     });
     const auto t1 = std::chrono::steady_clock::now();
     *seconds = std::chrono::duration<double>(t1 - t0).count();
-    *units_done = static_cast<int64_t>(heads) * units_per_head;
   });
 }
 

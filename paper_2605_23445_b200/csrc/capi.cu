@@ -1,0 +1,792 @@
+// capi.cu — the extern "C" boundary (include/dfs_gpu.h): handle, workspaces,
+// permutation cache, device mask cache and the Alg. 1 step driver.
+//
+// Host logic restated from the reference:
+//   SparsitySchedule  scheduler.cpp:18-56 (floor warmup, ceil phase length,
+//                     last phase absorbs, update every Delta sparse steps)
+//   MaskCache         scheduler.cpp:58-83 (per (layer, head), keeps the K of
+//                     its update step across phase changes — test_cli.cpp:279-283)
+//   should_update     scheduler.cpp:85-89
+//   run_step          scheduler.cpp:91-135 (dense steps skip the reorder)
+// The per-head loop of the reference becomes one batched launch per kernel over
+// all H heads of the layer; the unpermute is fused into the attention epilogue.
+#include <algorithm>
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+
+namespace dfsgpu {
+
+// ---- kernels implemented in the other translation units -------------------
+int order_tokens_impl(int ordering, int64_t f, int64_t h, int64_t w, uint32_t* fwd, uint32_t* inv,
+                      int* scratch, int64_t scratch_ints, cudaStream_t stream);
+int64_t order_tokens_scratch_ints(int ordering, int64_t f, int64_t h, int64_t w);
+int invert_permutation_impl(const uint32_t* fwd, int64_t n, uint32_t* inv, cudaStream_t stream);
+int validate_permutation_impl(const uint32_t* fwd, int64_t n, int* seen, int* bad, int* ok_host,
+                              cudaStream_t stream);
+int permute_rows_impl(const void* src, int src_layout, void* dst, int dst_layout, int dtype,
+                      const uint32_t* idx, int64_t n, int64_t heads, int64_t d, float* pooled,
+                      int64_t pool, int32_t* nonfinite, bool scatter, cudaStream_t stream);
+int finite_check_impl(const void* x, int64_t count, int dtype, int32_t* flag, cudaStream_t stream);
+int score_blocks_generic(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
+                         int64_t sub_block, double* S, float* P_ws, int64_t P_ws_floats, cudaStream_t stream);
+int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
+                       int64_t sub_block, double* S, void* ws, int64_t ws_bytes, cudaStream_t stream);
+bool score_sm100_supports(int64_t d, int64_t block, int64_t sub_block);
+int64_t score_sm100_ws_bytes(int64_t heads, int64_t n, int64_t d, int64_t block, int64_t sub_block);
+int topk_select_impl(const double* scores, int64_t heads, int64_t m, int64_t k, int32_t* lut, uint8_t* sel,
+                     uint8_t* bits, cudaStream_t stream);
+int64_t topk_max_m();
+int mask_bits_to_csr_impl(const uint8_t* bits, int64_t heads, int64_t m, int32_t* blk_ptr, int32_t* blk_idx,
+                          int32_t* counts_ws, int32_t* flag_ws, int64_t* nnz_host, cudaStream_t stream);
+int lut_row_ptr_impl(int64_t heads, int64_t m, int64_t k, int32_t* blk_ptr, cudaStream_t stream);
+int sparse_attn_generic(const dfs_attn_args& a, float scale, cudaStream_t stream);
+int sparse_attn_sm100(const dfs_attn_args& a, float scale, cudaStream_t stream);
+bool attn_sm100_supports(const dfs_attn_args& a);
+
+// ---- errors ----------------------------------------------------------------
+namespace {
+thread_local std::string g_error;
+}
+void set_error(const std::string& msg) { g_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  g_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return DFS_E_CUDA;
+}
+
+// ---- device buffers ---------------------------------------------------------
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  Buf() = default;
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  Buf(Buf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  Buf& operator=(Buf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+  int ensure(size_t need) {
+    if (need <= bytes) return DFS_OK;
+    if (p) {
+      cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+    }
+    if (need == 0) return DFS_OK;
+    DFS_CUDA_CHECK(cudaMalloc(&p, need));
+    bytes = need;
+    return DFS_OK;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace dfsgpu
+
+using namespace dfsgpu;
+
+struct PermEntry {
+  Buf fwd, inv;
+  int64_t n = 0;
+};
+
+struct HeadMask {
+  bool valid = false;
+  int last_update_step = 0;
+  int64_t nnz = 0;
+};
+
+// One layer's device-resident masks: a CSR over (head, query block).
+struct LayerMasks {
+  int64_t heads = 0, m = 0, block = 0;
+  Buf ptr, idx;  // ptr [heads*m+1], idx [cap]
+  std::vector<HeadMask> head;
+  std::vector<int64_t> head_off;  // start of each head's rows in idx
+};
+
+struct dfs_handle {
+  int device = 0;
+  std::map<std::tuple<int, int64_t, int64_t, int64_t>, PermEntry> perms;
+  std::map<int, LayerMasks> masks;  // keyed by layer
+  // workspaces
+  Buf scratch_i32, flag;
+  Buf q_hnd, k_hnd, v_hnd, pooled_q, pooled_k, scores, score_ws, lut, sel, counts;
+  Buf tmp_ptr, tmp_idx;
+  int64_t total_bytes() const {
+    int64_t t = 0;
+    for (const Buf* b : {&scratch_i32, &flag, &q_hnd, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
+                         &lut, &sel, &counts, &tmp_ptr, &tmp_idx})
+      t += int64_t(b->bytes);
+    return t;
+  }
+};
+
+namespace capi_detail {
+
+int check_handle(dfs_handle* h) {
+  if (!h) return fail(DFS_E_INVALID, "null dfs_handle");
+  DFS_CUDA_CHECK(cudaSetDevice(h->device));
+  return DFS_OK;
+}
+
+int schedule_validate(const dfs_schedule* s, int* warmup, int* phase_len) {
+  constexpr double kEps = 1e-9;  // scheduler.cpp:10-13
+  if (!s) return fail(DFS_E_INVALID, "null schedule");
+  if (s->total_steps < 1) return fail(DFS_E_INVALID, "SparsitySchedule: total_steps must be >= 1");
+  if (s->warmup_fraction < 0.0 || s->warmup_fraction > 1.0)
+    return fail(DFS_E_INVALID, "SparsitySchedule: warmup_fraction must lie in [0, 1]");
+  if (s->phase_fraction < 0.0 || s->phase_fraction > 1.0)
+    return fail(DFS_E_INVALID, "SparsitySchedule: phase_fraction must lie in [0, 1]");
+  if (s->update_interval < 1) return fail(DFS_E_INVALID, "SparsitySchedule: update_interval must be >= 1");
+  for (int i = 0; i < s->n_budgets; ++i)
+    if (!(s->phase_budgets[i] > 0.0) || s->phase_budgets[i] > 1.0)
+      return fail(DFS_E_INVALID, "SparsitySchedule: budgets must lie in (0, 1]");
+  if (s->warmup_fraction + double(s->n_budgets) * s->phase_fraction > 1.0 + kEps)
+    return fail(DFS_E_INVALID, "SparsitySchedule: warmup + phases exceed the step range");
+  const double t = double(s->total_steps);
+  int w = int(std::floor(s->warmup_fraction * t + kEps));
+  if (w > s->total_steps) w = s->total_steps;
+  if (w < s->total_steps && s->n_budgets == 0)
+    return fail(DFS_E_INVALID, "SparsitySchedule: sparse steps exist but no phase budgets given");
+  int pl = int(std::ceil(s->phase_fraction * t - kEps));
+  if (pl < 1) pl = 1;
+  if (warmup) *warmup = w;
+  if (phase_len) *phase_len = pl;
+  return DFS_OK;
+}
+
+int get_perm(dfs_handle* h, int ordering, int64_t f, int64_t hh, int64_t w, cudaStream_t stream,
+             const PermEntry** out) {
+  auto key = std::make_tuple(ordering, f, hh, w);
+  auto it = h->perms.find(key);
+  if (it == h->perms.end()) {
+    if (f < 1 || hh < 1 || w < 1) return fail(DFS_E_INVALID, "GridDims: extents must be >= 1");
+    PermEntry e;
+    e.n = f * hh * w;
+    int rc;
+    if ((rc = e.fwd.ensure(sizeof(uint32_t) * size_t(e.n)))) return rc;
+    if ((rc = e.inv.ensure(sizeof(uint32_t) * size_t(e.n)))) return rc;
+    const int64_t sc = order_tokens_scratch_ints(ordering, f, hh, w);
+    if ((rc = h->scratch_i32.ensure(sizeof(int) * size_t(sc)))) return rc;
+    if ((rc = order_tokens_impl(ordering, f, hh, w, e.fwd.as<uint32_t>(), e.inv.as<uint32_t>(),
+                                h->scratch_i32.as<int>(), sc, stream)))
+      return rc;
+    it = h->perms.emplace(key, std::move(e)).first;
+  }
+  *out = &it->second;
+  return DFS_OK;
+}
+
+float resolve_scale(float scale, int64_t d) { return scale > 0.f ? scale : float(1.0 / std::sqrt(double(d))); }
+
+int attn_dispatch(const dfs_attn_args& a, cudaStream_t stream) {
+  const float scale = resolve_scale(a.scale, a.d);
+  if (!a.force_generic && attn_sm100_supports(a)) return sparse_attn_sm100(a, scale, stream);
+  return sparse_attn_generic(a, scale, stream);
+}
+
+int score_dispatch(dfs_handle* h, const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d,
+                   int64_t block, int64_t sub, double* S, cudaStream_t stream) {
+  int rc;
+  if (score_sm100_supports(d, block, sub)) {
+    const int64_t need = score_sm100_ws_bytes(heads, n, d, block, sub);
+    if ((rc = h->score_ws.ensure(size_t(need)))) return rc;
+    return score_blocks_sm100(pq, pk, heads, n, d, block, sub, S, h->score_ws.p, need, stream);
+  }
+  const int64_t subs = block / sub;
+  const int64_t rows = ceil_div(n, block) * subs;
+  const int64_t per_head = rows * rows;
+  // batch as many heads as fit in 1 GiB of probability workspace (>= 1)
+  int64_t batch = (int64_t(1) << 28) / (per_head > 0 ? per_head : 1);
+  if (batch < 1) batch = 1;
+  if (batch > heads) batch = heads;
+  if ((rc = h->score_ws.ensure(sizeof(float) * size_t(batch * per_head)))) return rc;
+  return score_blocks_generic(pq, pk, heads, n, d, block, sub, S, h->score_ws.as<float>(),
+                              int64_t(h->score_ws.bytes / sizeof(float)), stream);
+}
+
+}  // namespace capi_detail
+using namespace capi_detail;
+
+extern "C" {
+
+const char* dfs_last_error(void) { return g_error.c_str(); }
+int dfs_abi_version(void) { return DFS_ABI_VERSION; }
+
+int dfs_handle_create(dfs_handle** out, int device) {
+  if (!out) return fail(DFS_E_INVALID, "null out");
+  int count = 0;
+  DFS_CUDA_CHECK(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(DFS_E_INVALID, "no such CUDA device");
+  DFS_CUDA_CHECK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  DFS_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(DFS_E_UNSUPPORTED, "this library is compiled for sm_100a (B200) only");
+  auto* h = new dfs_handle;
+  h->device = device;
+  if (int rc = h->flag.ensure(64)) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return DFS_OK;
+}
+
+int dfs_handle_destroy(dfs_handle* h) {
+  if (h) {
+    cudaSetDevice(h->device);
+    delete h;
+  }
+  return DFS_OK;
+}
+
+int dfs_handle_workspace_bytes(dfs_handle* h, int64_t* bytes) {
+  if (!h || !bytes) return fail(DFS_E_INVALID, "null argument");
+  *bytes = h->total_bytes();
+  return DFS_OK;
+}
+
+// ---------------------------------------------------------------- K1 -------
+int dfs_order_tokens(int ordering, int64_t f, int64_t h, int64_t w, uint32_t* fwd, uint32_t* inv,
+                     dfs_stream stream) {
+  if (f < 1 || h < 1 || w < 1) return fail(DFS_E_INVALID, "GridDims: extents must be >= 1");
+  if (f > (int64_t(1) << 31) / h / w) return fail(DFS_E_INVALID, "GridDims: token count overflows index range");
+  if (!fwd) return fail(DFS_E_INVALID, "null forward buffer");
+  const int64_t sc = order_tokens_scratch_ints(ordering, f, h, w);
+  int* scratch = nullptr;
+  DFS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(int) * size_t(sc), as_stream(stream)));
+  const int rc = order_tokens_impl(ordering, f, h, w, fwd, inv, scratch, sc, as_stream(stream));
+  cudaFreeAsync(scratch, as_stream(stream));
+  return rc;
+}
+
+int dfs_invert_permutation(const uint32_t* fwd, int64_t n, uint32_t* inv, dfs_stream stream) {
+  if (!fwd || !inv || n < 1) return fail(DFS_E_INVALID, "invert_permutation: bad arguments");
+  return invert_permutation_impl(fwd, n, inv, as_stream(stream));
+}
+
+int dfs_validate_permutation(dfs_handle* h, const uint32_t* fwd, int64_t n, int* ok_host, dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (!ok_host) return fail(DFS_E_INVALID, "null ok_host");
+  if (n < 1) {
+    *ok_host = 0;
+    return DFS_OK;
+  }
+  if (int rc = h->counts.ensure(sizeof(int) * size_t(n))) return rc;
+  return validate_permutation_impl(fwd, n, h->counts.as<int>(), h->flag.as<int>(), ok_host, as_stream(stream));
+}
+
+// ------------------------------------------------------------- K2 / K6 -----
+int dfs_permute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype, const uint32_t* idx,
+                     int64_t n, int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite,
+                     dfs_stream stream) {
+  if (!src || !dst || !idx) return fail(DFS_E_INVALID, "permute_rows: null pointer");
+  return permute_rows_impl(src, src_layout, dst, dst_layout, dtype, idx, n, heads, d, pooled, pool, nonfinite,
+                           false, as_stream(stream));
+}
+
+int dfs_unpermute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype, const uint32_t* idx,
+                       int64_t n, int64_t heads, int64_t d, dfs_stream stream) {
+  if (!src || !dst || !idx) return fail(DFS_E_INVALID, "unpermute_rows: null pointer");
+  return permute_rows_impl(src, src_layout, dst, dst_layout, dtype, idx, n, heads, d, nullptr, 1, nullptr, true,
+                           as_stream(stream));
+}
+
+// ------------------------------------------------------------- K3 / K4 -----
+int dfs_score_blocks(dfs_handle* h, const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d,
+                     int64_t block, int64_t sub_block, double* scores, dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (sub_block < 1 || block < sub_block)
+    return fail(DFS_E_INVALID, "ScoringParams: need 1 <= sub_block_size <= block_size");
+  if (block % sub_block) return fail(DFS_E_INVALID, "ScoringParams: sub_block_size must divide block_size");
+  if (n < 1 || heads < 1 || d < 1) return fail(DFS_E_INVALID, "score_blocks: empty input");
+  return score_dispatch(h, pq, pk, heads, n, d, block, sub_block, scores, as_stream(stream));
+}
+
+int dfs_topk_count(double budget, int64_t m, int64_t* k) {
+  if (!(budget > 0.0) || budget > 1.0) return fail(DFS_E_INVALID, "budget must lie in (0, 1]");
+  if (!k) return fail(DFS_E_INVALID, "null k");
+  int64_t kk = std::llround(budget * double(m));  // mask_builder.cpp:85, half away from zero
+  if (kk < 1) kk = 1;
+  if (kk > m) kk = m;
+  *k = kk;
+  return DFS_OK;
+}
+
+int dfs_topk_select(const double* scores, int64_t heads, int64_t m, int64_t k, int32_t* lut, uint8_t* bits,
+                    dfs_stream stream) {
+  if (!scores || m < 1 || heads < 1) return fail(DFS_E_INVALID, "topk_select: scores must be square and non-empty");
+  uint8_t* sel = nullptr;
+  cudaStream_t s = as_stream(stream);
+  if (bits) DFS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sel), size_t(heads * m * m), s));
+  const int rc = topk_select_impl(scores, heads, m, k, lut, sel, bits, s);
+  if (sel) cudaFreeAsync(sel, s);
+  return rc;
+}
+
+int dfs_mask_bits_to_csr(dfs_handle* h, const uint8_t* bits, int64_t heads, int64_t m, int32_t* blk_ptr,
+                         int32_t* blk_idx, int64_t* nnz_host, dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (int rc = h->counts.ensure(sizeof(int32_t) * size_t(heads * m))) return rc;
+  return mask_bits_to_csr_impl(bits, heads, m, blk_ptr, blk_idx, h->counts.as<int32_t>(), h->flag.as<int32_t>(),
+                               nnz_host, as_stream(stream));
+}
+
+int dfs_lut_row_ptr(int64_t heads, int64_t m, int64_t k, int32_t* blk_ptr, dfs_stream stream) {
+  return lut_row_ptr_impl(heads, m, k, blk_ptr, as_stream(stream));
+}
+
+// ---------------------------------------------------------------- K5 -------
+int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (!a || !a->q || !a->k || !a->v || !a->o) return fail(DFS_E_INVALID, "sparse_attn: null pointer");
+  if (a->nq < 1 || a->nk < 1 || a->d < 1 || a->heads < 1)
+    return fail(DFS_E_INVALID, "attention: empty input");
+  if (a->block < 1) return fail(DFS_E_INVALID, "block_size must be >= 1");
+  if ((a->blk_ptr == nullptr) != (a->blk_idx == nullptr))
+    return fail(DFS_E_INVALID, "sparse_attn: blk_ptr and blk_idx must both be set or both be NULL");
+  return attn_dispatch(*a, as_stream(stream));
+}
+
+// ---------------------------------------------------------- schedule -------
+int dfs_schedule_info(const dfs_schedule* s, int* warmup_steps, int* phase_length) {
+  return schedule_validate(s, warmup_steps, phase_length);
+}
+
+int dfs_schedule_budget_at(const dfs_schedule* s, int step, double* budget) {
+  int w, pl;
+  if (int rc = schedule_validate(s, &w, &pl)) return rc;
+  if (step < 0 || step >= s->total_steps) return fail(DFS_E_RANGE, "budget_at: step out of range");
+  if (step < w) {
+    *budget = -1.0;
+    return DFS_OK;
+  }
+  int phase = (step - w) / pl;
+  if (phase > s->n_budgets - 1) phase = s->n_budgets - 1;
+  *budget = s->phase_budgets[phase];
+  return DFS_OK;
+}
+
+int dfs_schedule_is_update_step(const dfs_schedule* s, int step, int* is_update) {
+  int w, pl;
+  if (int rc = schedule_validate(s, &w, &pl)) return rc;
+  *is_update = step >= w && ((step - w) % s->update_interval) == 0;
+  return DFS_OK;
+}
+
+// ---------------------------------------------------------- mask cache -----
+int dfs_mask_cache_clear(dfs_handle* h) {
+  if (!h) return fail(DFS_E_INVALID, "null handle");
+  h->masks.clear();
+  return DFS_OK;
+}
+
+int dfs_mask_cache_contains(dfs_handle* h, int layer, int head, int* found) {
+  if (!h || !found) return fail(DFS_E_INVALID, "null argument");
+  auto it = h->masks.find(layer);
+  *found = it != h->masks.end() && head >= 0 && head < int(it->second.head.size()) &&
+           it->second.head[size_t(head)].valid;
+  return DFS_OK;
+}
+
+int dfs_mask_cache_size(dfs_handle* h, int64_t* n) {
+  if (!h || !n) return fail(DFS_E_INVALID, "null argument");
+  int64_t c = 0;
+  for (auto& kv : h->masks)
+    for (auto& hm : kv.second.head) c += hm.valid;
+  *n = c;
+  return DFS_OK;
+}
+
+}  // extern "C"
+
+namespace capi_detail {
+
+__global__ void csr_to_bits_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t m,
+                                   int64_t row0, uint8_t* __restrict__ sel) {
+  const int64_t u = blockIdx.x;
+  const int32_t b = ptr[row0 + u], e = ptr[row0 + u + 1];
+  for (int32_t t = b + threadIdx.x; t < e; t += blockDim.x) sel[u * m + idx[t]] = 1;
+}
+
+__global__ void pack_sel_kernel(const uint8_t* __restrict__ sel, int64_t total, uint8_t* __restrict__ bits) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b * 8 >= total) return;
+  uint8_t o = 0;
+  for (int j = 0; j < 8; ++j)
+    if (b * 8 + j < total && sel[b * 8 + j]) o |= uint8_t(1u << (7 - j));
+  bits[b] = o;
+}
+
+__global__ void fill_kernel(int32_t* __restrict__ dst, int64_t count, int32_t value) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = value;
+}
+
+__global__ void rebase_ptr_kernel(const int32_t* __restrict__ src, int64_t count, int32_t delta,
+                                  int32_t* __restrict__ dst) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = src[i] + delta;
+}
+
+// Rebuild layer L's CSR so that head `hh` holds (ptr_h [m+1] relative, idx_h [nnz]) and
+// every other valid head keeps its rows. Rare path (explicit stores, partial updates).
+int layer_replace_heads(dfs_handle* h, LayerMasks& L, const std::vector<int>& heads_new,
+                        const std::vector<const int32_t*>& ptr_new, const std::vector<const int32_t*>& idx_new,
+                        const std::vector<int64_t>& nnz_new, cudaStream_t s) {
+  const int64_t H = L.heads, m = L.m;
+  std::vector<int64_t> nnz(size_t(H), 0);
+  std::vector<int> src(size_t(H), -1);  // index into heads_new, or -1 = keep old
+  for (size_t j = 0; j < heads_new.size(); ++j) src[size_t(heads_new[j])] = int(j);
+  int64_t total = 0;
+  for (int64_t hh = 0; hh < H; ++hh) {
+    if (src[size_t(hh)] >= 0)
+      nnz[size_t(hh)] = nnz_new[size_t(src[size_t(hh)])];
+    else
+      nnz[size_t(hh)] = L.head[size_t(hh)].valid ? L.head[size_t(hh)].nnz : 0;
+    total += nnz[size_t(hh)];
+  }
+  Buf nptr, nidx;
+  int rc;
+  if ((rc = nptr.ensure(sizeof(int32_t) * size_t(H * m + 1)))) return rc;
+  if ((rc = nidx.ensure(sizeof(int32_t) * size_t(total > 0 ? total : 1)))) return rc;
+  DFS_CUDA_CHECK(cudaMemsetAsync(nptr.p, 0, sizeof(int32_t) * size_t(H * m + 1), s));
+  std::vector<int64_t> off(size_t(H), 0);
+  int64_t o = 0;
+  for (int64_t hh = 0; hh < H; ++hh) {
+    off[size_t(hh)] = o;
+    const int j = src[size_t(hh)];
+    if (j >= 0) {
+      rebase_ptr_kernel<<<unsigned(ceil_div(m + 1, 256)), 256, 0, s>>>(ptr_new[size_t(j)], m + 1, int32_t(o),
+                                                                         nptr.as<int32_t>() + hh * m);
+      if (nnz[size_t(hh)])
+        DFS_CUDA_CHECK(cudaMemcpyAsync(nidx.as<int32_t>() + o, idx_new[size_t(j)],
+                                       sizeof(int32_t) * size_t(nnz[size_t(hh)]), cudaMemcpyDeviceToDevice, s));
+    } else if (L.head[size_t(hh)].valid) {
+      const int64_t old = L.head_off[size_t(hh)];
+      rebase_ptr_kernel<<<unsigned(ceil_div(m + 1, 256)), 256, 0, s>>>(
+          L.ptr.as<int32_t>() + hh * m, m + 1, int32_t(o - old), nptr.as<int32_t>() + hh * m);
+      if (nnz[size_t(hh)])
+        DFS_CUDA_CHECK(cudaMemcpyAsync(nidx.as<int32_t>() + o, L.idx.as<int32_t>() + old,
+                                       sizeof(int32_t) * size_t(nnz[size_t(hh)]), cudaMemcpyDeviceToDevice, s));
+    } else {
+      // empty head: all its row pointers equal o (keeps the CSR monotone)
+      fill_kernel<<<unsigned(ceil_div(m + 1, 256)), 256, 0, s>>>(nptr.as<int32_t>() + hh * m, m + 1, int32_t(o));
+    }
+    o += nnz[size_t(hh)];
+  }
+  DFS_LAUNCH_CHECK("layer_replace_heads");
+  DFS_CUDA_CHECK(cudaStreamSynchronize(s));  // old buffers are freed below
+  std::swap(L.ptr.p, nptr.p);
+  std::swap(L.ptr.bytes, nptr.bytes);
+  std::swap(L.idx.p, nidx.p);
+  std::swap(L.idx.bytes, nidx.bytes);
+  L.head_off = off;
+  for (int64_t hh = 0; hh < H; ++hh) L.head[size_t(hh)].nnz = nnz[size_t(hh)];
+  (void)h;
+  return DFS_OK;
+}
+
+}  // namespace capi_detail
+using namespace capi_detail;
+
+extern "C" {
+
+int dfs_mask_cache_store(dfs_handle* h, int layer, int head, const uint8_t* bits, int64_t m, int64_t block,
+                         int step, dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (head < 0 || m < 1 || !bits) return fail(DFS_E_INVALID, "mask_cache_store: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  LayerMasks& L = h->masks[layer];
+  if (L.m != 0 && (L.m != m || L.block != block)) {
+    // a new geometry for this layer replaces every head's mask
+    h->masks.erase(layer);
+    return dfs_mask_cache_store(h, layer, head, bits, m, block, step, stream);
+  }
+  if (L.m == 0) {
+    L.m = m;
+    L.block = block;
+  }
+  if (int64_t(head) >= L.heads) {
+    // grow the head range; existing rows are preserved by the rebuild below
+    const int64_t H = int64_t(head) + 1;
+    LayerMasks grown;
+    grown.heads = H;
+    grown.m = m;
+    grown.block = block;
+    grown.head = L.head;
+    grown.head.resize(size_t(H));
+    grown.head_off = L.head_off;
+    grown.head_off.resize(size_t(H), 0);
+    if (L.heads > 0) {
+      // carry the old CSR into the grown layout by treating old heads as "new"
+      std::vector<int> hs;
+      std::vector<const int32_t*> ps, is;
+      std::vector<int64_t> ns;
+      Buf tmp_ptrs;
+      for (int64_t hh = 0; hh < L.heads; ++hh)
+        if (L.head[size_t(hh)].valid) {
+          hs.push_back(int(hh));
+          ps.push_back(L.ptr.as<int32_t>() + hh * m);  // absolute offsets; rebased below
+          is.push_back(L.idx.as<int32_t>());
+          ns.push_back(L.head[size_t(hh)].nnz);
+        }
+      // absolute pointers: rebasing by 0 and copying the whole old idx per head
+      // would be wrong, so rebuild through relative copies
+      std::vector<Buf> rel_ptr(hs.size());
+      for (size_t j = 0; j < hs.size(); ++j) {
+        const int64_t hh = hs[j];
+        if (int rc = rel_ptr[j].ensure(sizeof(int32_t) * size_t(m + 1))) return rc;
+        rebase_ptr_kernel<<<unsigned(ceil_div(m + 1, 256)), 256, 0, s>>>(
+            L.ptr.as<int32_t>() + hh * m, m + 1, -int32_t(L.head_off[size_t(hh)]), rel_ptr[j].as<int32_t>());
+        ps[j] = rel_ptr[j].as<int32_t>();
+        is[j] = L.idx.as<int32_t>() + L.head_off[size_t(hh)];
+      }
+      for (auto& hm : grown.head) hm.valid = false;
+      if (int rc = layer_replace_heads(h, grown, hs, ps, is, ns, s)) return rc;
+      for (size_t j = 0; j < hs.size(); ++j) grown.head[size_t(hs[j])] = L.head[size_t(hs[j])];
+      for (int64_t hh = 0; hh < H; ++hh)
+        if (!grown.head[size_t(hh)].valid) grown.head[size_t(hh)].nnz = 0;
+    } else {
+      if (int rc = grown.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))) return rc;
+      DFS_CUDA_CHECK(cudaMemsetAsync(grown.ptr.p, 0, sizeof(int32_t) * size_t(H * m + 1), s));
+      if (int rc = grown.idx.ensure(sizeof(int32_t))) return rc;
+    }
+    L = std::move(grown);
+  }
+  // bits -> relative CSR for this head
+  Buf ptr1, idx1;
+  int64_t nnz = 0;
+  if (int rc = ptr1.ensure(sizeof(int32_t) * size_t(m + 1))) return rc;
+  if (int rc = idx1.ensure(sizeof(int32_t) * size_t(m * m))) return rc;
+  if (int rc = dfs_mask_bits_to_csr(h, bits, 1, m, ptr1.as<int32_t>(), idx1.as<int32_t>(), &nnz, stream)) return rc;
+  if (int rc = layer_replace_heads(h, L, {head}, {ptr1.as<int32_t>()}, {idx1.as<int32_t>()}, {nnz}, s)) return rc;
+  L.head[size_t(head)].valid = true;
+  L.head[size_t(head)].last_update_step = step;
+  return DFS_OK;
+}
+
+int dfs_mask_cache_get(dfs_handle* h, int layer, int head, uint8_t* bits, int* last_update_step, int64_t* m,
+                       dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  auto it = h->masks.find(layer);
+  if (it == h->masks.end() || head < 0 || head >= int(it->second.head.size()) ||
+      !it->second.head[size_t(head)].valid)
+    return fail(DFS_E_INVALID, "mask_cache_get: no entry for (layer, head)");
+  LayerMasks& L = it->second;
+  if (m) *m = L.m;
+  if (last_update_step) *last_update_step = L.head[size_t(head)].last_update_step;
+  if (!bits) return DFS_OK;
+  cudaStream_t s = as_stream(stream);
+  uint8_t* sel = nullptr;
+  DFS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&sel), size_t(L.m * L.m), s));
+  DFS_CUDA_CHECK(cudaMemsetAsync(sel, 0, size_t(L.m * L.m), s));
+  csr_to_bits_kernel<<<unsigned(L.m), 64, 0, s>>>(L.ptr.as<int32_t>(), L.idx.as<int32_t>(), L.m,
+                                                 int64_t(head) * L.m, sel);
+  const int64_t bytes = (L.m * L.m + 7) / 8;
+  pack_sel_kernel<<<unsigned(ceil_div(bytes, 256)), 256, 0, s>>>(sel, L.m * L.m, bits);
+  cudaFreeAsync(sel, s);
+  DFS_LAUNCH_CHECK("mask_cache_get");
+  return DFS_OK;
+}
+
+// ------------------------------------------------------------ run_step -----
+int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* a, dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (!a || !a->q || !a->k || !a->v || !a->o) return fail(DFS_E_INVALID, "run_step: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int64_t n = a->n, H = a->heads, d = a->d, B = a->block, Bs = a->sub_block;
+  if (n < 1 || H < 1 || d < 1) return fail(DFS_E_INVALID, "attention: empty input");
+  if (Bs < 1 || B < Bs) return fail(DFS_E_INVALID, "ScoringParams: need 1 <= sub_block_size <= block_size");
+  if (B % Bs) return fail(DFS_E_INVALID, "ScoringParams: sub_block_size must divide block_size");
+  double budget;
+  if (int rc = dfs_schedule_budget_at(sched, a->step, &budget)) return rc;
+  const int64_t m = ceil_div(n, B);
+
+  if (budget < 0.0 || a->force_dense) {  // scheduler.cpp:99-105: dense, raster order, no reorder
+    if (a->nonfinite)
+      for (const void* x : {a->q, a->k, a->v})
+        if (int rc = finite_check_impl(x, n * H * d, DFS_BF16, a->nonfinite, s)) return rc;
+    dfs_attn_args at{};
+    at.q = a->q;
+    at.k = a->k;
+    at.v = a->v;
+    at.o = a->o;
+    at.dtype = DFS_BF16;
+    at.in_layout = DFS_NHD;
+    at.out_layout = DFS_NHD;
+    at.heads = H;
+    at.nq = n;
+    at.nk = n;
+    at.d = d;
+    at.block = B;
+    if (int rc = attn_dispatch(at, s)) return rc;
+    if (a->dense_out) *a->dense_out = 1;
+    if (a->budget_out) *a->budget_out = 1.0;
+    for (int64_t hh = 0; hh < H; ++hh) {
+      if (a->updated_out) a->updated_out[hh] = 0;
+      if (a->sparsity_out) a->sparsity_out[hh] = 0.0;
+    }
+    return DFS_OK;
+  }
+
+  // sparse: reorder
+  const uint32_t* fwd = a->perm;
+  if (!fwd) {
+    const PermEntry* pe;
+    if (int rc = get_perm(h, DFS_HILBERT3D, a->frames, a->height, a->width, s, &pe)) return rc;
+    if (pe->n != n) return fail(DFS_E_INVALID, "run_step: permutation length does not match token count");
+    fwd = pe->fwd.as<uint32_t>();
+  }
+  // which heads need a fresh mask (scheduler.cpp:85-89)
+  int is_upd = 0;
+  dfs_schedule_is_update_step(sched, a->step, &is_upd);
+  LayerMasks* L = nullptr;
+  {
+    auto it = h->masks.find(a->layer);
+    if (it != h->masks.end()) {
+      if (it->second.m != m || it->second.block != B || it->second.heads != H)
+        h->masks.erase(it);  // geometry changed: nothing reusable
+      else
+        L = &it->second;
+    }
+  }
+  std::vector<int> need;
+  for (int64_t hh = 0; hh < H; ++hh)
+    if (is_upd || !L || !L->head[size_t(hh)].valid) need.push_back(int(hh));
+  const bool update_any = !need.empty();
+
+  int rc;
+  const size_t tok_bytes = sizeof(__nv_bfloat16) * size_t(n * H * d);
+  if ((rc = h->q_hnd.ensure(tok_bytes)) || (rc = h->k_hnd.ensure(tok_bytes)) || (rc = h->v_hnd.ensure(tok_bytes)))
+    return rc;
+  const int64_t pv = ceil_div(n, Bs);
+  float* pq = nullptr;
+  float* pk = nullptr;
+  if (update_any) {
+    if ((rc = h->pooled_q.ensure(sizeof(float) * size_t(H * pv * d))) ||
+        (rc = h->pooled_k.ensure(sizeof(float) * size_t(H * pv * d))))
+      return rc;
+    pq = h->pooled_q.as<float>();
+    pk = h->pooled_k.as<float>();
+  }
+  if ((rc = permute_rows_impl(a->q, DFS_NHD, h->q_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pq, Bs, a->nonfinite,
+                              false, s)) ||
+      (rc = permute_rows_impl(a->k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, Bs, a->nonfinite,
+                              false, s)) ||
+      (rc = permute_rows_impl(a->v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, a->nonfinite,
+                              false, s)))
+    return rc;
+
+  if (update_any) {
+    int64_t K;
+    if ((rc = dfs_topk_count(budget, m, &K))) return rc;
+    if ((rc = h->scores.ensure(sizeof(double) * size_t(H * m * m)))) return rc;
+    if ((rc = score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s))) return rc;
+    if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large");
+    if (int(need.size()) == H) {
+      // common case: every head refreshes -> the LUT becomes the layer's CSR in place
+      LayerMasks& NL = h->masks[a->layer];
+      NL.heads = H;
+      NL.m = m;
+      NL.block = B;
+      NL.head.assign(size_t(H), HeadMask{});
+      NL.head_off.resize(size_t(H));
+      if ((rc = NL.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))) ||
+          (rc = NL.idx.ensure(sizeof(int32_t) * size_t(H * m * K))))
+        return rc;
+      if ((rc = topk_select_impl(h->scores.as<double>(), H, m, K, NL.idx.as<int32_t>(), nullptr, nullptr, s)))
+        return rc;
+      if ((rc = lut_row_ptr_impl(H, m, K, NL.ptr.as<int32_t>(), s))) return rc;
+      for (int64_t hh = 0; hh < H; ++hh) {
+        NL.head[size_t(hh)] = HeadMask{true, a->step, m * K};
+        NL.head_off[size_t(hh)] = hh * m * K;
+      }
+      L = &NL;
+    } else {
+      if ((rc = h->lut.ensure(sizeof(int32_t) * size_t(H * m * K))) ||
+          (rc = h->tmp_ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))))
+        return rc;
+      if ((rc = topk_select_impl(h->scores.as<double>(), H, m, K, h->lut.as<int32_t>(), nullptr, nullptr, s)))
+        return rc;
+      if ((rc = lut_row_ptr_impl(1, m, K, h->tmp_ptr.as<int32_t>(), s))) return rc;
+      LayerMasks& NL = h->masks[a->layer];
+      if (NL.m == 0) {
+        NL.heads = H;
+        NL.m = m;
+        NL.block = B;
+        NL.head.assign(size_t(H), HeadMask{});
+        NL.head_off.assign(size_t(H), 0);
+        if ((rc = NL.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1)))) return rc;
+        DFS_CUDA_CHECK(cudaMemsetAsync(NL.ptr.p, 0, sizeof(int32_t) * size_t(H * m + 1), s));
+      }
+      std::vector<const int32_t*> ps, is;
+      std::vector<int64_t> ns;
+      for (int hh : need) {
+        ps.push_back(h->tmp_ptr.as<int32_t>());
+        is.push_back(h->lut.as<int32_t>() + int64_t(hh) * m * K);
+        ns.push_back(m * K);
+      }
+      if ((rc = layer_replace_heads(h, NL, need, ps, is, ns, s))) return rc;
+      for (int hh : need) {
+        NL.head[size_t(hh)].valid = true;
+        NL.head[size_t(hh)].last_update_step = a->step;
+      }
+      L = &NL;
+    }
+  }
+
+  dfs_attn_args at{};
+  at.q = h->q_hnd.p;
+  at.k = h->k_hnd.p;
+  at.v = h->v_hnd.p;
+  at.o = a->o;
+  at.dtype = DFS_BF16;
+  at.in_layout = DFS_HND;
+  at.out_layout = DFS_NHD;
+  at.heads = H;
+  at.nq = n;
+  at.nk = n;
+  at.d = d;
+  at.block = B;
+  at.blk_ptr = L->ptr.as<int32_t>();
+  at.blk_idx = L->idx.as<int32_t>();
+  at.out_rows = fwd;  // fused unpermute: row i -> raster row fwd[i] (scheduler.cpp:134)
+  if ((rc = attn_dispatch(at, s))) return rc;
+
+  if (a->dense_out) *a->dense_out = 0;
+  if (a->budget_out) *a->budget_out = budget;
+  for (int64_t hh = 0; hh < H; ++hh) {
+    const bool upd = std::find(need.begin(), need.end(), int(hh)) != need.end();
+    if (a->updated_out) a->updated_out[hh] = upd;
+    if (a->sparsity_out) a->sparsity_out[hh] = 1.0 - double(L->head[size_t(hh)].nnz) / (double(m) * double(m));
+  }
+  return DFS_OK;
+}
+
+}  // extern "C"

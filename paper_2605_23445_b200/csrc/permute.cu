@@ -1,0 +1,195 @@
+// permute.cu — K2 (gather + fused mean-pool + finite check) and K6 (scatter).
+//
+// apply_permutation (curve.cpp:166-176) is a row gather out[i] = x[fwd[i]];
+// here it runs for every head at once and converts [N,H,d] raster activations
+// to the path's head-major [H,N,d] reordered layout. Pure data movement:
+// HBM-bound, so every access is a 16-byte vector, the source row (H*d*2 bytes
+// per token, 6 KB at HunyuanVideo) is read by consecutive threads, and each
+// thread keeps `kUnroll` independent row loads in flight.
+//
+// When the destination rows are also needed as sub-block means for scoring
+// (mask_builder.cpp:12-28 mean_pool: fp64 accumulate, divide by B_s even for
+// the zero-padded last group, fp32 store) the CTA owns whole pooling groups and
+// emits the pooled rows from registers: the scores never re-read Q/K.
+#include "common.cuh"
+
+namespace dfsgpu {
+
+namespace {
+
+template <typename T>
+struct Vec;  // 16-byte vector of T
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+};
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+};
+
+template <typename T>
+__device__ __forceinline__ void unpack(const uint4& u, float (&x)[Vec<T>::N]);
+template <>
+__device__ __forceinline__ void unpack<float>(const uint4& u, float (&x)[4]) {
+  x[0] = __uint_as_float(u.x);
+  x[1] = __uint_as_float(u.y);
+  x[2] = __uint_as_float(u.z);
+  x[3] = __uint_as_float(u.w);
+}
+template <>
+__device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& u, float (&x)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    x[2 * j] = __uint_as_float(w[j] << 16);
+    x[2 * j + 1] = __uint_as_float(w[j] & 0xffff0000u);
+  }
+}
+
+// One CTA = `rows` consecutive destination rows (a pooling group when pooling)
+// x all heads. Thread slots walk (head, 16B column chunk).
+template <typename T, bool kPool, bool kScatter>
+__global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ src, int src_layout,
+                                                      T* __restrict__ dst, int dst_layout,
+                                                      const uint32_t* __restrict__ idx, int64_t n,
+                                                      int64_t heads, int64_t d, int rows,
+                                                      float* __restrict__ pooled, int64_t pool,
+                                                      int32_t* __restrict__ nonfinite) {
+  constexpr int V = Vec<T>::N;
+  const int64_t vec_per_row = d / V;
+  const int64_t slots = heads * vec_per_row;
+  const int64_t r0 = int64_t(blockIdx.x) * rows;
+  bool bad = false;
+  for (int64_t s = threadIdx.x; s < slots; s += blockDim.x) {
+    const int64_t h = s / vec_per_row;
+    const int64_t c = (s % vec_per_row) * V;
+    double acc[kPool ? V : 1];
+    if (kPool) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] = 0.0;
+    }
+#pragma unroll 4
+    for (int r = 0; r < rows; ++r) {
+      const int64_t i = r0 + r;
+      if (i >= n) break;
+      // gather: read source row idx[i] -> write dest row i; scatter: the reverse
+      const int64_t si = kScatter ? i : int64_t(idx[i]);
+      const int64_t di = kScatter ? int64_t(idx[i]) : i;
+      const uint4 u = *reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c);
+      *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) = u;
+      if (kPool || nonfinite) {
+        float x[V];
+        unpack<T>(u, x);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if (kPool) acc[j] += double(x[j]);
+          bad |= !isfinite(x[j]);
+        }
+      }
+    }
+    if (kPool) {
+      const int64_t g = r0 / pool;
+      float* out = pooled + (h * ceil_div(n, pool) + g) * d + c;
+#pragma unroll
+      for (int j = 0; j < V; ++j) out[j] = float(acc[j] / double(pool));
+    }
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+// scalar fallback for d not a multiple of the 16-byte vector (drop-in shapes)
+template <typename T, bool kScatter>
+__global__ void permute_scalar_kernel(const T* __restrict__ src, int src_layout, T* __restrict__ dst,
+                                      int dst_layout, const uint32_t* __restrict__ idx, int64_t n,
+                                      int64_t heads, int64_t d, float* __restrict__ pooled,
+                                      int64_t pool, int32_t* __restrict__ nonfinite) {
+  // one CTA per pooling group (or per 16 rows), one thread per (head, column)
+  const int64_t rows = pooled ? pool : 16;
+  const int64_t r0 = int64_t(blockIdx.x) * rows;
+  bool bad = false;
+  for (int64_t s = threadIdx.x; s < heads * d; s += blockDim.x) {
+    const int64_t h = s / d, c = s % d;
+    double acc = 0.0;
+    for (int64_t r = 0; r < rows; ++r) {
+      const int64_t i = r0 + r;
+      if (i >= n) break;
+      const int64_t si = kScatter ? i : int64_t(idx[i]);
+      const int64_t di = kScatter ? int64_t(idx[i]) : i;
+      const T x = src[row_offset(src_layout, n, heads, d, h, si) + c];
+      dst[row_offset(dst_layout, n, heads, d, h, di) + c] = x;
+      const float xf = to_f32<T>(x);
+      acc += double(xf);
+      bad |= !isfinite(xf);
+    }
+    if (pooled) pooled[(h * ceil_div(n, pool) + r0 / pool) * d + c] = float(acc / double(pool));
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+template <typename T, bool kScatter>
+int launch(const void* src, int src_layout, void* dst, int dst_layout, const uint32_t* idx, int64_t n,
+           int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite, cudaStream_t stream) {
+  const T* s = static_cast<const T*>(src);
+  T* o = static_cast<T*>(dst);
+  const bool vec_ok = d % Vec<T>::N == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (!pooled || pool <= 64);
+  const int64_t rows = pooled ? pool : 16;
+  const int64_t grid = ceil_div(n, rows);
+  if (grid > int64_t(INT32_MAX)) return fail(DFS_E_UNSUPPORTED, "permute: too many rows");
+  if (vec_ok) {
+    if (pooled)
+      permute_kernel<T, true, kScatter><<<unsigned(grid), 256, 0, stream>>>(
+          s, src_layout, o, dst_layout, idx, n, heads, d, int(rows), pooled, pool, nonfinite);
+    else
+      permute_kernel<T, false, kScatter><<<unsigned(grid), 256, 0, stream>>>(
+          s, src_layout, o, dst_layout, idx, n, heads, d, int(rows), nullptr, 1, nonfinite);
+  } else {
+    permute_scalar_kernel<T, kScatter><<<unsigned(grid), 256, 0, stream>>>(
+        s, src_layout, o, dst_layout, idx, n, heads, d, pooled, pool, nonfinite);
+  }
+  DFS_LAUNCH_CHECK("permute_rows");
+  return DFS_OK;
+}
+
+template <typename T>
+__global__ void finite_kernel(const T* __restrict__ x, int64_t count, int32_t* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+    bad |= !isfinite(to_f32<T>(x[i]));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+}  // namespace
+
+// attention.cpp:19-20 (non-finite input is an error) for the dense-step path
+int finite_check_impl(const void* x, int64_t count, int dtype, int32_t* flag, cudaStream_t stream) {
+  const int64_t blocks = ceil_div(count, 256) < 8 * kNumSMs ? ceil_div(count, 256) : 8 * kNumSMs;
+  if (dtype == DFS_BF16)
+    finite_kernel<<<unsigned(blocks), 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(x), count, flag);
+  else
+    finite_kernel<<<unsigned(blocks), 256, 0, stream>>>(static_cast<const float*>(x), count, flag);
+  DFS_LAUNCH_CHECK("finite_check");
+  return DFS_OK;
+}
+
+int permute_rows_impl(const void* src, int src_layout, void* dst, int dst_layout, int dtype,
+                      const uint32_t* idx, int64_t n, int64_t heads, int64_t d, float* pooled,
+                      int64_t pool, int32_t* nonfinite, bool scatter, cudaStream_t stream) {
+  if (n < 1 || heads < 1 || d < 1) return fail(DFS_E_INVALID, "permute_rows: empty input");
+  if (pooled && pool < 1) return fail(DFS_E_INVALID, "mean_pool: pool must be >= 1");
+  if (pooled && scatter) return fail(DFS_E_INVALID, "permute_rows: pooling only on gather");
+  if (dtype == DFS_BF16)
+    return scatter ? launch<__nv_bfloat16, true>(src, src_layout, dst, dst_layout, idx, n, heads, d, pooled,
+                                                 pool, nonfinite, stream)
+                   : launch<__nv_bfloat16, false>(src, src_layout, dst, dst_layout, idx, n, heads, d,
+                                                  pooled, pool, nonfinite, stream);
+  if (dtype == DFS_F32)
+    return scatter ? launch<float, true>(src, src_layout, dst, dst_layout, idx, n, heads, d, pooled, pool,
+                                         nonfinite, stream)
+                   : launch<float, false>(src, src_layout, dst, dst_layout, idx, n, heads, d, pooled, pool,
+                                          nonfinite, stream);
+  return fail(DFS_E_INVALID, "permute_rows: unknown dtype");
+}
+
+}  // namespace dfsgpu
