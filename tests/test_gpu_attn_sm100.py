@@ -1,0 +1,122 @@
+"""K5 tcgen05 kernel parity: against the oracle (fp64, the reference's
+arithmetic) on sampled rows, and against the geometry-generic SIMT kernel on
+full tensors. bf16 I/O tolerance: max|O - O_ref| / max|O_ref| <= 2e-2 per head
+(SURVEY.md §8(d)); observed errors are ~3e-3."""
+import numpy as np
+import pytest
+
+from oracle import ora
+
+from tests.golden.make_golden import bf16_round
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def dfs():
+    import paper_2605_23445_b200 as m
+
+    return m
+
+
+def rel(o, ref):
+    return float((o - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+
+
+def random_lut(h, mq, mk, k, gen):
+    idx = torch.stack([torch.stack([torch.randperm(mk, generator=gen)[:k].sort().values for _ in range(mq)])
+                       for _ in range(h)])
+    return idx.to(torch.int32)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("n,k", [(128, 1), (1000, 3), (4096 + 77, 7), (17550, 28)])
+def test_sm100_matches_generic_hnd_lut(d, n, k):
+    m = dfs()
+    gen = torch.Generator().manual_seed(n * d + k)
+    h = 3
+    q, kk, v = (torch.randn(h, n, d, generator=gen).to(torch.bfloat16).cuda() for _ in range(3))
+    mq = -(-n // 128)
+    k = min(k, mq)
+    lut = random_lut(h, mq, mq, k, gen).cuda()
+    ptr = m.ops.lut_row_ptr(h, mq, k)
+    o_fast = m.sparse_attention_csr(q, kk, v, ptr, lut.reshape(-1), 128)
+    o_ref = m.sparse_attention_csr(q, kk, v, ptr, lut.reshape(-1), 128, force_generic=True)
+    torch.cuda.synchronize()
+    for hh in range(h):
+        assert rel(o_fast[hh].float(), o_ref[hh].float()) <= 1e-2, hh
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_sm100_dense_nhd_and_cross_attention(d):
+    m = dfs()
+    gen = torch.Generator().manual_seed(7 + d)
+    h, nq, nk = 2, 777, 1500
+    q = torch.randn(nq, h, d, generator=gen).to(torch.bfloat16).cuda()
+    k = torch.randn(nk, h, d, generator=gen).to(torch.bfloat16).cuda()
+    v = torch.randn(nk, h, d, generator=gen).to(torch.bfloat16).cuda()
+    o = m.full_attention_output(q, k, v)  # Nq != Nk through K5 with a full mask
+    og = m.full_attention_output(q, k, v, force_generic=True)
+    assert rel(o.float(), og.float()) <= 1e-2
+    qf, kf, vf = (x.float().cpu().numpy() for x in (q, k, v))
+    for hh in range(h):
+        ref = ora.full_attention_output(qf[:, hh], kf[:, hh], vf[:, hh], rows=(0, 200))
+        got = o[:200, hh].float().cpu()
+        assert rel(got, torch.from_numpy(ref[:200])) <= 2e-2
+
+
+def test_sm100_scatter_epilogue_matches_unpermute():
+    """out_rows fuses the inverse permutation (scheduler.cpp:134) into K5's epilogue."""
+    m = dfs()
+    dims = (13, 30, 45)
+    n, h, d = 13 * 30 * 45, 4, 64
+    gen = torch.Generator().manual_seed(3)
+    q, k, v = (torch.randn(h, n, d, generator=gen).to(torch.bfloat16).cuda() for _ in range(3))
+    perm = m.hilbert3d_order(dims)
+    mq = -(-n // 128)
+    lut = random_lut(h, mq, mq, 28, gen).cuda()
+    ptr = m.ops.lut_row_ptr(h, mq, 28)
+    o_hnd = m.sparse_attention_csr(q, k, v, ptr, lut.reshape(-1), 128)           # reordered [H, N, d]
+    o_nhd = m.sparse_attention_csr(q, k, v, ptr, lut.reshape(-1), 128, out_layout=0,
+                                   out_rows=perm.forward)                         # raster [N, H, d]
+    want = m.unpermute(perm, o_hnd.transpose(0, 1).contiguous())
+    assert torch.equal(o_nhd, want)
+
+
+@pytest.mark.slow
+def test_sm100_hunyuan_two_heads_vs_oracle_rows():
+    """HY geometry (118,800 tokens, d=128, K=93 of 929): smooth inputs, real
+    top-K masks from the GPU scorer, sampled rows against the fp64 oracle."""
+    m = dfs()
+    dims, d = (33, 45, 80), 128
+    n = 33 * 45 * 80
+    heads = []
+    for h in range(2):
+        q, k, v = (bf16_round(x) for x in ora.gen_video_field(dims, d, 4.0, ora.derive_seed(1, [0, h])))
+        heads.append((q, k, v))
+    Q, K, V = (torch.from_numpy(np.stack([hd[i] for hd in heads], 1)).to(torch.bfloat16).cuda() for i in range(3))
+    perm = m.hilbert3d_order(dims)
+    qh, pq = m.ops.permute_to_hnd(Q, perm, 16)
+    kh, pk = m.ops.permute_to_hnd(K, perm, 16)
+    vh, _ = m.ops.permute_to_hnd(V, perm, 0)
+    S = m.ops.score_pooled(pq, pk, n, m.ScoringParams(128, 16))
+    lut = m.topk_lut(S, 0.1)
+    assert lut.shape == (2, 929, 93)
+    ptr = m.ops.lut_row_ptr(2, 929, 93)
+    o = m.sparse_attention_csr(qh, kh, vh, ptr, lut.reshape(-1), 128)
+    fwd = perm.forward.cpu().numpy().astype(np.uint32)
+    rows = np.r_[0:256, 60000:60128, n - 144:n]
+    for h in range(2):
+        rq, rk, rv = (ora.apply_permutation(fwd, x) for x in heads[h])
+        dense = np.zeros((929, 929), bool)
+        dense[np.arange(929)[:, None], lut[h].cpu().numpy()] = True
+        from oracle import dense_to_mask_bits
+
+        bits = dense_to_mask_bits(dense)
+        ref = np.zeros((n, d), np.float32)
+        for lo, hi in [(0, 256), (60000, 60128), (n - 144, n)]:
+            ref[lo:hi] = ora.block_sparse_attention(rq, rk, rv, bits, 929, 128, rows=(lo, hi))[lo:hi]
+        got = o[h].float().cpu().numpy()[rows]
+        err = np.abs(got - ref[rows]).max() / np.abs(ref[rows]).max()
+        assert err <= 2e-2, (h, err)
