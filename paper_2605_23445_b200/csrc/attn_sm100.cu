@@ -62,6 +62,7 @@ struct Params {
   const uint32_t* out_rows;
   __nv_bfloat16* out;
   int out_layout;
+  int in_nhd;  // 1: inputs are [N, H, d] (tensor-map coordinates (col, head, row))
   float scale_log2;
   int64_t tiles;
 };
@@ -142,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* dst = sRing + slot * C::kTileBytes;
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(dst + c * C::kChunkBytes, map, &bars->kv_full[slot], c * 64, int(row0), int(h));
+          tma_load_3d(dst + c * C::kChunkBytes, map, &bars->kv_full[slot], c * 64, p.in_nhd ? int(h) : int(row0),
+                      p.in_nhd ? int(row0) : int(h));
         ++ring;
       };
       for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
@@ -154,7 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&bars->q_full, C::kTileBytes);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(sQ + c * C::kChunkBytes, &tm_q, &bars->q_full, c * 64, int(u * kBM), int(h));
+          tma_load_3d(sQ + c * C::kChunkBytes, &tm_q, &bars->q_full, c * 64, p.in_nhd ? int(h) : int(u * kBM),
+                      p.in_nhd ? int(u * kBM) : int(h));
         // consumption order of the MMA warp: K0, K1, V0, K2, V1, ..., V_{n-1}
         load_tile(&tm_k, h, int64_t(block_at(p, beg, 0)) * kBN);
         for (int32_t j = 1; j < cnt; ++j) {
@@ -265,9 +268,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           o_phase ^= 1;
           tc_fence_after();
         }
+        // tcgen05.ld/st are warp-collective (.sync.aligned): the rescale decision
+        // must be warp-uniform, so one lagging row rescales its whole warp
         if (j == 0) {
           m = m_new;
-        } else if (m_new - m > kRescaleThreshold) {
+        } else if (__any_sync(0xffffffffu, m_new - m > kRescaleThreshold)) {
           const float alpha = ex2(m - m_new);
           l *= alpha;
           m = m_new;
@@ -411,6 +416,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream, int layout_
   p.out_rows = a.out_rows;
   p.out = static_cast<__nv_bfloat16*>(a.o);
   p.out_layout = a.out_layout;
+  p.in_nhd = a.in_layout == DFS_NHD;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.tiles = p.mq * a.heads;
   static bool attr_set = false;
