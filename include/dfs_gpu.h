@@ -206,6 +206,11 @@ typedef struct {
 } dfs_step_args;
 int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
 
+/* Per-handle kernel selection (A/B tests): route scoring / attention through
+ * the geometry-generic kernels even where the tcgen05 ones apply. */
+enum dfs_option { DFS_OPT_GENERIC_SCORE = 1, DFS_OPT_GENERIC_ATTN = 2 };
+int dfs_handle_set_option(dfs_handle* h, int option, int value);
+
 /* Device mem introspection for the bench (bytes of workspace held). */
 int dfs_handle_workspace_bytes(dfs_handle* h, int64_t* bytes);
 

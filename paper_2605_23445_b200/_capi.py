@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libdfs_b200.so")
 DFS_OK, DFS_E_INVALID, DFS_E_RANGE, DFS_E_UNSUPPORTED, DFS_E_CUDA, DFS_E_INTERNAL = 0, -1, -2, -3, -4, -5
 DFS_BF16, DFS_F32 = 0, 1
 DFS_NHD, DFS_HND = 0, 1
+DFS_OPT_GENERIC_SCORE, DFS_OPT_GENERIC_ATTN = 1, 2
 ORDERINGS = {"raster": 0, "hilbert2d": 1, "block3d": 2, "hilbert3d": 3}
 
 if not os.path.exists(LIB_PATH):
@@ -59,6 +60,7 @@ _SIGS = {
     "dfs_handle_create": (_i32, [C.POINTER(_p), _i32]),
     "dfs_handle_destroy": (_i32, [_p]),
     "dfs_handle_workspace_bytes": (_i32, [_p, C.POINTER(_i64)]),
+    "dfs_handle_set_option": (_i32, [_p, _i32, _i32]),
     "dfs_order_tokens": (_i32, [_i32, _i64, _i64, _i64, _p, _p, _p]),
     "dfs_invert_permutation": (_i32, [_p, _i64, _p, _p]),
     "dfs_validate_permutation": (_i32, [_p, _p, _i64, C.POINTER(_i32), _p]),

@@ -130,6 +130,8 @@ struct LayerMasks {
 
 struct dfs_handle {
   int device = 0;
+  int opt_generic_score = 0;  // DFS_OPT_GENERIC_SCORE
+  int opt_generic_attn = 0;   // DFS_OPT_GENERIC_ATTN
   std::map<std::tuple<int, int64_t, int64_t, int64_t>, PermEntry> perms;
   std::map<int, LayerMasks> masks;  // keyed by layer
   // workspaces
@@ -203,16 +205,16 @@ int get_perm(dfs_handle* h, int ordering, int64_t f, int64_t hh, int64_t w, cuda
 
 float resolve_scale(float scale, int64_t d) { return scale > 0.f ? scale : float(1.0 / std::sqrt(double(d))); }
 
-int attn_dispatch(const dfs_attn_args& a, cudaStream_t stream) {
+int attn_dispatch(dfs_handle* h, const dfs_attn_args& a, cudaStream_t stream) {
   const float scale = resolve_scale(a.scale, a.d);
-  if (!a.force_generic && attn_sm100_supports(a)) return sparse_attn_sm100(a, scale, stream);
+  if (!a.force_generic && !h->opt_generic_attn && attn_sm100_supports(a)) return sparse_attn_sm100(a, scale, stream);
   return sparse_attn_generic(a, scale, stream);
 }
 
 int score_dispatch(dfs_handle* h, const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d,
                    int64_t block, int64_t sub, double* S, cudaStream_t stream) {
   int rc;
-  if (score_sm100_supports(d, block, sub)) {
+  if (!h->opt_generic_score && score_sm100_supports(d, block, sub)) {
     const int64_t need = score_sm100_ws_bytes(heads, n, d, block, sub);
     if ((rc = h->score_ws.ensure(size_t(need)))) return rc;
     return score_blocks_sm100(pq, pk, heads, n, d, block, sub, S, h->score_ws.p, need, stream);
@@ -263,6 +265,20 @@ int dfs_handle_destroy(dfs_handle* h) {
     delete h;
   }
   return DFS_OK;
+}
+
+int dfs_handle_set_option(dfs_handle* h, int option, int value) {
+  if (!h) return fail(DFS_E_INVALID, "null handle");
+  switch (option) {
+    case DFS_OPT_GENERIC_SCORE:
+      h->opt_generic_score = value;
+      return DFS_OK;
+    case DFS_OPT_GENERIC_ATTN:
+      h->opt_generic_attn = value;
+      return DFS_OK;
+    default:
+      return fail(DFS_E_INVALID, "unknown handle option");
+  }
 }
 
 int dfs_handle_workspace_bytes(dfs_handle* h, int64_t* bytes) {
@@ -370,7 +386,7 @@ int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream
   if (a->block < 1) return fail(DFS_E_INVALID, "block_size must be >= 1");
   if ((a->blk_ptr == nullptr) != (a->blk_idx == nullptr))
     return fail(DFS_E_INVALID, "sparse_attn: blk_ptr and blk_idx must both be set or both be NULL");
-  return attn_dispatch(*a, as_stream(stream));
+  return attn_dispatch(h, *a, as_stream(stream));
 }
 
 // ---------------------------------------------------------- schedule -------
@@ -645,7 +661,7 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     at.nk = n;
     at.d = d;
     at.block = B;
-    if (int rc = attn_dispatch(at, s)) return rc;
+    if (int rc = attn_dispatch(h, at, s)) return rc;
     if (a->dense_out) *a->dense_out = 1;
     if (a->budget_out) *a->budget_out = 1.0;
     for (int64_t hh = 0; hh < H; ++hh) {
@@ -777,7 +793,7 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   at.blk_ptr = L->ptr.as<int32_t>();
   at.blk_idx = L->idx.as<int32_t>();
   at.out_rows = fwd;  // fused unpermute: row i -> raster row fwd[i] (scheduler.cpp:134)
-  if ((rc = attn_dispatch(at, s))) return rc;
+  if ((rc = attn_dispatch(h, at, s))) return rc;
 
   if (a->dense_out) *a->dense_out = 0;
   if (a->budget_out) *a->budget_out = budget;

@@ -1,13 +1,354 @@
-// score_sm100.cu — K3 tensor-core path (placeholder until the tcgen05 kernel lands).
+// score_sm100.cu — K3 tensor-core path: hierarchical block scores on tcgen05.
+//
+// mask_builder.cpp:30-80 (+ attention.cpp:105-123 as the pooled softmax):
+//   S[u][v] = sum over the subs x subs tile (u, v) of softmax_row(Q^ K^T / sqrt(d))
+// with Q^, K^ the sub-block means (fp32, from K2's fused pooling). The survey
+// (SURVEY.md §0 finding 4) shows scores sit within 1e-4..1e-7 of each other at
+// the top-K cut, so the pooled GEMM must be fp32-accurate: bf16/TF32 operands
+// flip 0.03-1% of mask bits. Here every fp32 operand is split into two fp16
+// halves after a per-head power-of-two scaling (so both halves are normal):
+//   a*s = hi + lo * 2^-11,   hi = f16(a*s),  lo = f16((a*s - hi) * 2^11)
+//   Q^K^T * sq*sk = Qhi Khi^T + 2^-11 (Qhi Klo^T + Qlo Khi^T)   (+ O(2^-22))
+// three fp16 UMMAs at the full 16-bit tensor rate (twice TF32's), fp32
+// accumulation in TMEM: D1 = hi*hi, D2 = the two cross terms.
+//
+// One CTA per (head, 128 pooled query rows); two passes over the 128-wide
+// pooled key tiles: pass 0 the row max / partition function, pass 1 the fp32
+// probabilities summed over `subs` columns in registers and over `subs` rows
+// with warp shuffles, written as fp64 S entries. Warp roles as in K5: warp 0
+// TMA, warp 1 MMA issue, warps 2-5 one pooled row per thread (= TMEM lane).
+// Padded query rows are zero vectors (uniform over the valid keys, mask_builder
+// .cpp:40-49); padded key columns are excluded (:50-60).
+#include <cuda.h>
+#include <cuda_fp16.h>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace dfsgpu {
 
-bool score_sm100_supports(int64_t, int64_t, int64_t) { return false; }
-int64_t score_sm100_ws_bytes(int64_t, int64_t, int64_t, int64_t, int64_t) { return 0; }
-int score_blocks_sm100(const float*, const float*, int64_t, int64_t, int64_t, int64_t, int64_t, double*, void*,
-                       int64_t, cudaStream_t) {
-  return fail(DFS_E_UNSUPPORTED, "score_blocks_sm100: not built");
+int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d);
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kRows = 128;
+constexpr int kKeys = 128;
+constexpr int kThreads = 192;
+constexpr float kLoScale = 2048.f;        // 2^11
+constexpr float kInvLoScale = 1.f / 2048.f;
+
+template <int D>
+struct SCfg {
+  static constexpr int kChunks = D / 64;
+  static constexpr int kChunkBytes = 128 * 128;          // 128 rows x 64 fp16
+  static constexpr int kOpBytes = kRows * D * 2;          // one hi or lo operand tile
+  static constexpr int kStages = D == 64 ? 4 : 2;
+  static constexpr int kQOff = 0;                         // Qhi, Qlo
+  static constexpr int kKOff = 2 * kOpBytes;              // stages x (Khi, Klo)
+  static constexpr int kBarOff = kKOff + kStages * 2 * kOpBytes;
+  static constexpr int kSmem = kBarOff + 256 + 1024;
+};
+
+// kind::f16 with fp16 inputs (formats 0), fp32 accumulation, K-major A and B
+constexpr uint32_t kIdesc = (1u << 4) | (uint32_t(kKeys >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
+
+struct SParams {
+  int64_t heads, qvalid, kvalid, m, subs, nrt, nkt, items;
+  const float* fac;   // [H]: scale_log2 / (sq * sk)
+  double* S;
+};
+
+struct SBars {
+  uint64_t q_full, q_empty;
+  uint64_t k_full[4], k_empty[4];
+  uint64_t acc_full[2], acc_free[2];
+  uint32_t tmem_base;
+};
+
+template <int D, int SUBS>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_sm100_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
+                       const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
+                       const SParams p) {
+  using C = SCfg<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  SBars* bars = reinterpret_cast<SBars*>(smem + C::kBarOff);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->q_empty, 1);
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&bars->k_full[i], 1);
+      mbar_init(&bars->k_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->acc_full[i], 1);
+      mbar_init(&bars->acc_free[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t q_phase = 0, ring = 0;
+      for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
+        const int h = int(it / p.nrt), rt = int(it % p.nrt);
+        mbar_wait(&bars->q_empty, q_phase ^ 1);
+        q_phase ^= 1;
+        mbar_expect_tx(&bars->q_full, 2 * C::kOpBytes);
+        for (int c = 0; c < C::kChunks; ++c) {
+          tma_load_3d(smem + C::kQOff + c * C::kChunkBytes, &tm_qh, &bars->q_full, c * 64, rt * kRows, h);
+          tma_load_3d(smem + C::kQOff + C::kOpBytes + c * C::kChunkBytes, &tm_ql, &bars->q_full, c * 64, rt * kRows, h);
+        }
+        for (int pass = 0; pass < 2; ++pass)
+          for (int kt = 0; kt < p.nkt; ++kt) {
+            const uint32_t slot = ring % C::kStages;
+            mbar_wait(&bars->k_empty[slot], ((ring / C::kStages) & 1) ^ 1);
+            mbar_expect_tx(&bars->k_full[slot], 2 * C::kOpBytes);
+            uint8_t* dst = smem + C::kKOff + slot * 2 * C::kOpBytes;
+            for (int c = 0; c < C::kChunks; ++c) {
+              tma_load_3d(dst + c * C::kChunkBytes, &tm_kh, &bars->k_full[slot], c * 64, kt * kKeys, h);
+              tma_load_3d(dst + C::kOpBytes + c * C::kChunkBytes, &tm_kl, &bars->k_full[slot], c * 64, kt * kKeys, h);
+            }
+            ++ring;
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t q_phase = 0, ring = 0, acc_iter = 0;
+      const uint32_t qh = smem_u32(smem + C::kQOff), ql = qh + C::kOpBytes;
+      for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
+        mbar_wait(&bars->q_full, q_phase);
+        q_phase ^= 1;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int kt = 0; kt < p.nkt; ++kt) {
+            const uint32_t slot = ring % C::kStages;
+            mbar_wait(&bars->k_full[slot], (ring / C::kStages) & 1);
+            ++ring;
+            const uint32_t b = acc_iter & 1;
+            mbar_wait(&bars->acc_free[b], ((acc_iter >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t kh = smem_u32(smem + C::kKOff + slot * 2 * C::kOpBytes), kl = kh + C::kOpBytes;
+            const uint32_t d1 = tmem + b * 256, d2 = d1 + 128;
+#pragma unroll
+            for (int s = 0; s < D / 16; ++s) {
+              const uint32_t off = (s >> 2) * C::kChunkBytes + (s & 3) * 32;
+              umma_f16(d1, smem_desc_sw128(qh + off, 16, 1024), smem_desc_sw128(kh + off, 16, 1024), kIdesc, s > 0);
+              umma_f16(d2, smem_desc_sw128(qh + off, 16, 1024), smem_desc_sw128(kl + off, 16, 1024), kIdesc, s > 0);
+              umma_f16(d2, smem_desc_sw128(ql + off, 16, 1024), smem_desc_sw128(kh + off, 16, 1024), kIdesc, 1);
+            }
+            umma_commit(&bars->k_empty[slot]);
+            umma_commit(&bars->acc_full[b]);
+            if (pass == 1 && kt == p.nkt - 1) umma_commit(&bars->q_empty);
+            ++acc_iter;
+          }
+      }
+    }
+  } else {
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
+    uint32_t acc_iter = 0;
+    for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
+      const int h = int(it / p.nrt), rt = int(it % p.nrt);
+      const float f = p.fac[h];
+      const int64_t row = int64_t(rt) * kRows + r;     // pooled query row
+      const int64_t u = row / SUBS;
+      float m = -INFINITY, z = 0.f, inv_z = 0.f;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int kt = 0; kt < p.nkt; ++kt) {
+          const uint32_t b = acc_iter & 1;
+          mbar_wait(&bars->acc_full[b], (acc_iter >> 1) & 1);
+          tc_fence_after();
+          const int64_t col0 = int64_t(kt) * kKeys;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t a1[32], a2[32];
+            tmem_ld32(tmem + lane_addr + b * 256 + c * 32, a1);
+            tmem_ld32(tmem + lane_addr + b * 256 + 128 + c * 32, a2);
+            tmem_wait_ld();
+            if (c == 3) {
+              tc_fence_before();
+              mbar_arrive(&bars->acc_free[b]);
+            }
+            float l[32];
+            const int64_t cbase = col0 + c * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float x = fmaf(__uint_as_float(a2[i]), kInvLoScale, __uint_as_float(a1[i])) * f;
+              l[i] = (cbase + i < p.kvalid) ? x : -INFINITY;
+            }
+            if (pass == 0) {
+              float mx = l[0];
+#pragma unroll
+              for (int i = 1; i < 32; ++i) mx = fmaxf(mx, l[i]);
+              const float mn = fmaxf(m, mx);
+              if (mn > -INFINITY) {
+                float s = 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) s += ex2(l[i] - mn);
+                z = z * ex2(m - mn) + s;
+                m = mn;
+              }
+            } else {
+              // probabilities (fp32, attention.cpp:120), summed over SUBS columns, then SUBS rows
+#pragma unroll
+              for (int g = 0; g < 32 / SUBS; ++g) {
+                float t = 0.f;
+#pragma unroll
+                for (int i = 0; i < SUBS; ++i) t += ex2(l[g * SUBS + i] - m) * inv_z;
+#pragma unroll
+                for (int o = 1; o < SUBS; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                const int64_t v = (cbase + g * SUBS) / SUBS;
+                if ((lane % SUBS) == 0 && u < p.m && v < p.m) p.S[(int64_t(h) * p.m + u) * p.m + v] = double(t);
+              }
+            }
+          }
+          ++acc_iter;
+        }
+        if (pass == 0) inv_z = 1.f / z;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// ---- operand preparation: per-head power-of-two scale, fp16 hi/lo split ----------
+
+__global__ void absmax_kernel(const float* __restrict__ x, int64_t per_head, int heads, unsigned* __restrict__ out) {
+  const int h = blockIdx.y;
+  float mx = 0.f;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_head; i += int64_t(gridDim.x) * blockDim.x)
+    mx = fmaxf(mx, fabsf(x[h * per_head + i]));
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(out + h, __float_as_uint(mx));
+}
+
+__device__ __forceinline__ float pow2_scale(unsigned bits) {
+  // largest power of two s with max|x| * s <= 2^14 (both halves stay normal fp16)
+  const float mx = __uint_as_float(bits);
+  if (!(mx > 0.f) || !isfinite(mx)) return 1.f;
+  int e;
+  frexpf(mx, &e);  // mx = f * 2^e, f in [0.5, 1)
+  return ldexpf(1.f, 14 - e);
+}
+
+__global__ void split_kernel(const float* __restrict__ x, int64_t per_head, const unsigned* __restrict__ amax,
+                             __half* __restrict__ hi, __half* __restrict__ lo) {
+  const int h = blockIdx.y;
+  const float s = pow2_scale(amax[h]);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_head; i += int64_t(gridDim.x) * blockDim.x) {
+    const float a = x[h * per_head + i] * s;
+    const __half hh = __float2half_rn(a);
+    hi[h * per_head + i] = hh;
+    lo[h * per_head + i] = __float2half_rn((a - __half2float(hh)) * kLoScale);
+  }
+}
+
+__global__ void factor_kernel(const unsigned* __restrict__ amax_q, const unsigned* __restrict__ amax_k, int heads,
+                              float scale_log2, float* __restrict__ fac) {
+  const int h = threadIdx.x + blockIdx.x * blockDim.x;
+  if (h < heads) fac[h] = scale_log2 / (pow2_scale(amax_q[h]) * pow2_scale(amax_k[h]));
+}
+
+template <int D, int SUBS>
+int launch(const CUtensorMap* maps, const SParams& p, cudaStream_t stream) {
+  using C = SCfg<D>;
+  static bool attr = false;
+  if (!attr) {
+    DFS_CUDA_CHECK(cudaFuncSetAttribute(score_sm100_kernel<D, SUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C::kSmem));
+    attr = true;
+  }
+  const int64_t grid = p.items < kNumSMs ? p.items : kNumSMs;
+  score_sm100_kernel<D, SUBS><<<unsigned(grid), kThreads, C::kSmem, stream>>>(maps[0], maps[1], maps[2], maps[3], p);
+  DFS_LAUNCH_CHECK("score_sm100");
+  return DFS_OK;
+}
+
+}  // namespace
+
+bool score_sm100_supports(int64_t d, int64_t block, int64_t sub_block) {
+  if (d != 64 && d != 128) return false;
+  if (sub_block < 1 || block % sub_block) return false;
+  const int64_t subs = block / sub_block;
+  return subs == 2 || subs == 4 || subs == 8 || subs == 16 || subs == 32;
+}
+
+int64_t score_sm100_ws_bytes(int64_t heads, int64_t n, int64_t d, int64_t block, int64_t sub_block) {
+  (void)block;
+  const int64_t valid = ceil_div(n, sub_block);
+  return 4 * heads * valid * d * 2 /* qh ql kh kl */ + 2 * heads * 4 /* absmax */ + heads * 4 /* fac */ + 256;
+}
+
+int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
+                       int64_t sub_block, double* S, void* ws, int64_t ws_bytes, cudaStream_t stream) {
+  if (ws_bytes < score_sm100_ws_bytes(heads, n, d, block, sub_block))
+    return fail(DFS_E_INTERNAL, "score_sm100: workspace too small");
+  const int64_t valid = ceil_div(n, sub_block);
+  const int64_t per_head = valid * d;
+  __half* qh = static_cast<__half*>(ws);
+  __half* ql = qh + heads * per_head;
+  __half* kh = ql + heads * per_head;
+  __half* kl = kh + heads * per_head;
+  unsigned* amax = reinterpret_cast<unsigned*>(kl + heads * per_head);
+  float* fac = reinterpret_cast<float*>(amax + 2 * heads);
+  DFS_CUDA_CHECK(cudaMemsetAsync(amax, 0, sizeof(unsigned) * size_t(2 * heads), stream));
+  dim3 g(unsigned(ceil_div(per_head, 256) < 64 ? ceil_div(per_head, 256) : 64), unsigned(heads));
+  absmax_kernel<<<g, 256, 0, stream>>>(pq, per_head, int(heads), amax);
+  absmax_kernel<<<g, 256, 0, stream>>>(pk, per_head, int(heads), amax + heads);
+  split_kernel<<<g, 256, 0, stream>>>(pq, per_head, amax, qh, ql);
+  split_kernel<<<g, 256, 0, stream>>>(pk, per_head, amax + heads, kh, kl);
+  const float scale_log2 = float(1.4426950408889634 / sqrt(double(d)));
+  factor_kernel<<<1, 256, 0, stream>>>(amax, amax + heads, int(heads), scale_log2, fac);
+  DFS_LAUNCH_CHECK("score_sm100 prep");
+
+  CUtensorMap maps[4];
+  int rc;
+  if ((rc = make_map_f16(&maps[0], qh, valid, heads, d)) || (rc = make_map_f16(&maps[1], ql, valid, heads, d)) ||
+      (rc = make_map_f16(&maps[2], kh, valid, heads, d)) || (rc = make_map_f16(&maps[3], kl, valid, heads, d)))
+    return rc;
+  SParams p;
+  p.heads = heads;
+  p.qvalid = valid;
+  p.kvalid = valid;
+  p.m = ceil_div(n, block);
+  p.subs = block / sub_block;
+  p.nrt = ceil_div(p.m * p.subs, kRows);
+  p.nkt = ceil_div(valid, kKeys);
+  p.items = heads * p.nrt;
+  p.fac = fac;
+  p.S = S;
+  const int subs = int(p.subs);
+  if (d == 128) {
+    switch (subs) {
+      case 2: return launch<128, 2>(maps, p, stream);
+      case 4: return launch<128, 4>(maps, p, stream);
+      case 8: return launch<128, 8>(maps, p, stream);
+      case 16: return launch<128, 16>(maps, p, stream);
+      case 32: return launch<128, 32>(maps, p, stream);
+    }
+  } else {
+    switch (subs) {
+      case 2: return launch<64, 2>(maps, p, stream);
+      case 4: return launch<64, 4>(maps, p, stream);
+      case 8: return launch<64, 8>(maps, p, stream);
+      case 16: return launch<64, 16>(maps, p, stream);
+      case 32: return launch<64, 32>(maps, p, stream);
+    }
+  }
+  return fail(DFS_E_UNSUPPORTED, "score_sm100: unsupported geometry");
 }
 
 }  // namespace dfsgpu

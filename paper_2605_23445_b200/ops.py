@@ -50,6 +50,9 @@ class Handle:
         except Exception:
             pass
 
+    def set_option(self, option: int, value: int) -> None:
+        capi.call("dfs_handle_set_option", self.ptr, int(option), int(value))
+
     def workspace_bytes(self) -> int:
         n = C.c_int64()
         capi.call("dfs_handle_workspace_bytes", self.ptr, C.byref(n))
