@@ -131,17 +131,36 @@ def test_topk_bit_exact_given_reference_scores(golden):
                 assert (got[h] == lut_o).all(), (m_, gam, h)
 
 
+class generic_scorer:
+    """Route block scoring through the fp64 geometry-generic kernel (handle option)."""
+
+    def __enter__(self):
+        dfs().default_handle().set_option(1, 1)
+
+    def __exit__(self, *exc):
+        dfs().default_handle().set_option(1, 0)
+
+
 def test_scores_and_masks_small_cases(golden):
+    """fp64 generic scorer: 1e-9 and bit-exact masks; tcgen05 scorer (d in {64,128}):
+    1e-4 and >= 99.5% mask agreement."""
     g = golden("kats")
     for i in g["cases"]:
         n, d, b, bs, gam = g[f"c{i}_meta"]
         n, d, b, bs = int(n), int(d), int(b), int(bs)
         q, k = g[f"c{i}_q"], g[f"c{i}_k"]
-        S = host(dfs().block_scores(cu(q), cu(k), dfs().ScoringParams(b, bs)))
         ref = g[f"c{i}_S"]
-        assert np.abs(S - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), i
+        with generic_scorer():
+            S = host(dfs().block_scores(cu(q), cu(k), dfs().ScoringParams(b, bs)))
+            assert np.abs(S - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max()), i
+            mask = dfs().build_mask(cu(q), cu(k), dfs().ScoringParams(b, bs), float(gam))
+            assert (host(mask.bits) == g[f"c{i}_bits"]).all(), i
+        S = host(dfs().block_scores(cu(q), cu(k), dfs().ScoringParams(b, bs)))
+        assert np.abs(S - ref).max() <= 1e-4 * np.abs(ref).max(), i
+        mm = ref.shape[0]
         mask = dfs().build_mask(cu(q), cu(k), dfs().ScoringParams(b, bs), float(gam))
-        assert (host(mask.bits) == g[f"c{i}_bits"]).all(), i
+        agree = (mask_bits_to_dense(host(mask.bits), mm) == mask_bits_to_dense(g[f"c{i}_bits"], mm)).mean()
+        assert agree >= 0.995, (i, agree)
 
 
 def test_tiny_config_scores(golden):
@@ -149,10 +168,14 @@ def test_tiny_config_scores(golden):
     for h in range(2):
         rq = ora.apply_permutation(g["fwd"], g[f"q{h}"])
         rk = ora.apply_permutation(g["fwd"], g[f"k{h}"])
-        S = host(dfs().block_scores(cu(rq), cu(rk), dfs().ScoringParams(64, 16)))
+        with generic_scorer():
+            S = host(dfs().block_scores(cu(rq), cu(rk), dfs().ScoringParams(64, 16)))
         assert np.abs(S - g[f"S{h}"]).max() <= 1e-9
         mask = dfs().topk_select(cu(S), 0.5, 64)
         assert (host(mask.bits) == g[f"bits{h}"]).all()
+        S2 = host(dfs().block_scores(cu(rq), cu(rk), dfs().ScoringParams(64, 16)))
+        assert np.abs(S2 - g[f"S{h}"]).max() <= 1e-4 * np.abs(g[f"S{h}"]).max()
+        assert (host(dfs().topk_select(cu(S2), 0.5, 64).bits) == g[f"bits{h}"]).all()
 
 
 # ------------------------------------------------------------------ K5 -----
