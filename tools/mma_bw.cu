@@ -1,0 +1,115 @@
+// tools/mma_bw.cu — microbenchmark: tcgen05.mma throughput per SM for the K5 shapes
+// (M=128, N=128, K=16 bf16; SS = both operands in smem, TS = A in TMEM), with and
+// without concurrent TMA traffic into shared memory.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/mma_bw tools/mma_bw.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdio.h>
+
+#include "../paper_2605_23445_b200/csrc/sm100.cuh"
+
+using namespace dfsgpu::sm100;
+
+__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int mode, int n_dim, unsigned long long* out,
+                                                       const __grid_constant__ CUtensorMap map, int tma) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t tbase;
+  __shared__ uint64_t bar, tbar[2];
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&tbar[0], 1);
+    mbar_init(&tbar[1], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  const uint32_t a = smem_u32(smem), b = a + 32768;
+  const uint32_t idesc = idesc_bf16_f32(128, n_dim, false, false);
+  unsigned long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) {
+    t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
+        if (mode == 0)
+          umma_f16(tmem + (it & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024), idesc,
+                   s > 0);
+        else
+          umma_f16_ts(tmem + (it & 1) * 128, tmem + 384 + s * 8, smem_desc_sw128(b + off, 16, 1024), idesc, s > 0);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  } else if (threadIdx.x == 32 && tma) {
+    // concurrent TMA stream into a separate 2 x 32 KB region (L2-resident source)
+    uint8_t* dst = smem + 65536;
+    for (int t = 0; t < tma; ++t) {
+      const int slot = t & 1;
+      if (t >= 2) mbar_wait(&tbar[slot], ((t >> 1) - 1) & 1);
+      mbar_expect_tx(&tbar[slot], 32768);
+      tma_load_3d(dst + slot * 32768, &map, &tbar[slot], 0, (t * 7 % 900) * 128, 0);
+      tma_load_3d(dst + slot * 32768 + 16384, &map, &tbar[slot], 64, (t * 7 % 900) * 128, 0);
+    }
+    for (int t = (tma > 2 ? tma - 2 : 0); t < tma; ++t) mbar_wait(&tbar[t & 1], (t >> 1) & 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int main() {
+  void* ptr = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q);
+  EncodeFn enc = (EncodeFn)ptr;
+  void* buf;
+  const int rows = 118912;
+  cudaMalloc(&buf, size_t(rows) * 256);
+  cudaMemset(buf, 0, size_t(rows) * 256);
+  CUtensorMap map;
+  cuuint64_t dims[3] = {128, (cuuint64_t)rows, 1};
+  cuuint64_t strides[2] = {256, (cuuint64_t)rows * 256};
+  cuuint32_t box[3] = {64, 128, 1}, es[3] = {1, 1, 1};
+  enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * sizeof(unsigned long long));
+  const int smem = 65536 + 65536 + 1024;
+  cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 4000;
+  for (int mode = 0; mode < 2; ++mode)
+    for (int n : {128, 256})
+      for (int tma : {0, 2000, 6000}) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        mma_kernel<<<148, 128, smem>>>(iters, mode, n, d, map, tma);
+        cudaEventRecord(e0);
+        mma_kernel<<<148, 128, smem>>>(iters, mode, n, d, map, tma);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long c[148];
+        cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
+        const double flops = 2.0 * 128 * n * 16 * 8.0 * iters * 148;
+        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", mode ? "TS" : "SS", n, tma,
+               double(c[0]) / (iters * 8), ms, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+      }
+  return 0;
+}
