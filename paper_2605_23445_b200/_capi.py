@@ -12,7 +12,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdfs_b200.so")
+# DFS_B200_LIB points at an alternative build of the same library (A/B kernel measurements)
+LIB_PATH = os.environ.get("DFS_B200_LIB") or os.path.join(HERE, "libdfs_b200.so")
 
 DFS_OK, DFS_E_INVALID, DFS_E_RANGE, DFS_E_UNSUPPORTED, DFS_E_CUDA, DFS_E_INTERNAL = 0, -1, -2, -3, -4, -5
 DFS_BF16, DFS_F32 = 0, 1

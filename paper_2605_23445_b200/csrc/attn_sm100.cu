@@ -75,14 +75,13 @@ struct Params {
   int in_nhd;  // 1: inputs are [N, H, d] (tensor-map coordinates (col, head, row))
   float scale_log2;
   unsigned long long* trace;  // debug timeline (DFS_ATTN_TRACE), NULL in production
-  int exp_mode;               // debug (DFS_ATTN_EXP): 1 skip QK, 2 skip PV, 4 skip softmax math
   int64_t tiles;
 };
 
 struct Bars {
   uint64_t q_full, q_empty;
   uint64_t s_full[3];
-  uint64_t p_full, o_done;
+  uint64_t p_full[3], o_done[3];  // per S/P buffer: the softmax may run a block ahead of PV
   uint64_t kv_full[12], kv_empty[12];
   uint32_t tmem_base;
 };
@@ -100,21 +99,26 @@ __device__ __forceinline__ void tile_list(const Params& p, int64_t tile, int64_t
   }
 }
 
+#ifdef DFS_ATTN_TRACE_BUILD
 __device__ __forceinline__ void trace(const Params& p, int ev, uint32_t idx) {
   if (p.trace && blockIdx.x == 0 && idx < 256) p.trace[ev * 256 + idx] = clock64();
 }
+#else
+__device__ __forceinline__ void trace(const Params&, int, uint32_t) {}
+#endif
 
 __device__ __forceinline__ int32_t block_at(const Params& p, int32_t beg, int32_t j) {
   return p.blk_ptr ? p.blk_idx[beg + j] : j;
 }
 
-template <int D>
+template <int D, int POLY>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = Cfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SWIZZLE_128B atoms) by offset, so the pointer keeps its shared state space
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem + C::kQOff;
   uint8_t* sRing = smem + C::kRingOff;
   float* red = reinterpret_cast<float*>(smem + C::kRedOff);  // [parity][wg][row]
@@ -124,9 +128,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
     mbar_init(&bars->q_empty, 1);
-    for (int i = 0; i < 3; ++i) mbar_init(&bars->s_full[i], 1);
-    mbar_init(&bars->p_full, kSoftmaxThreads);
-    mbar_init(&bars->o_done, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&bars->s_full[i], 1);
+      mbar_init(&bars->p_full[i], kSoftmaxThreads);
+      mbar_init(&bars->o_done[i], 1);
+    }
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(&bars->kv_full[i], 1);
       mbar_init(&bars->kv_empty[i], 1);
@@ -146,107 +152,139 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ================================ TMA producer ==============================
-    if (lane == 0) {
-      uint32_t q_phase = 0, ring = 0;
-      auto load_tile = [&](const CUtensorMap* map, int64_t h, int64_t row0) {
-        const uint32_t slot = ring % C::kStages;
-        const uint32_t use = ring / C::kStages;
-        mbar_wait(&bars->kv_empty[slot], (use & 1) ^ 1);
+    // The whole warp runs the loop (so the control state is warp-uniform) and one
+    // elected lane issues; the key-block list is read 32 entries at a time by the
+    // warp (one coalesced load) and broadcast with shuffles, keeping the LUT's
+    // global-load latency off the per-block issue path.
+    uint32_t q_phase = 0, ring = 0;
+    auto load_tile = [&](const CUtensorMap* map, int64_t h, int64_t row0) {
+      const uint32_t slot = ring % C::kStages;
+      const uint32_t use = ring / C::kStages;
+      mbar_wait(&bars->kv_empty[slot], (use & 1) ^ 1);
+      if (elect_one()) {
         mbar_expect_tx(&bars->kv_full[slot], C::kTileBytes);
         uint8_t* dst = sRing + slot * C::kTileBytes;
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d(dst + c * C::kChunkBytes, map, &bars->kv_full[slot], c * 64, p.in_nhd ? int(h) : int(row0),
                       p.in_nhd ? int(row0) : int(h));
-        ++ring;
-      };
-      for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-        int64_t h, u;
-        int32_t beg, cnt;
-        tile_list(p, tile, h, u, beg, cnt);
-        mbar_wait(&bars->q_empty, q_phase ^ 1);
-        q_phase ^= 1;
+      }
+      __syncwarp();
+      ++ring;
+    };
+    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      int64_t h, u;
+      int32_t beg, cnt;
+      tile_list(p, tile, h, u, beg, cnt);
+      mbar_wait(&bars->q_empty, q_phase ^ 1);
+      q_phase ^= 1;
+      if (elect_one()) {
         mbar_expect_tx(&bars->q_full, C::kTileBytes);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
           tma_load_3d(sQ + c * C::kChunkBytes, &tm_q, &bars->q_full, c * 64, p.in_nhd ? int(h) : int(u * kBM),
                       p.in_nhd ? int(u * kBM) : int(h));
-        // consumption order of the MMA warp (QK runs two blocks ahead of PV):
-        // K0, K1, K2, V0, K3, V1, ..., K_{n-1}, V_{n-3}, V_{n-2}, V_{n-1}
-        load_tile(&tm_k, h, int64_t(block_at(p, beg, 0)) * kBN);
-        if (cnt > 1) load_tile(&tm_k, h, int64_t(block_at(p, beg, 1)) * kBN);
-        for (int32_t j = 0; j < cnt; ++j) {
-          if (j + 2 < cnt) load_tile(&tm_k, h, int64_t(block_at(p, beg, j + 2)) * kBN);
-          load_tile(&tm_v, h, int64_t(block_at(p, beg, j)) * kBN);
+      }
+      __syncwarp();
+      // key-block list window: entries [win, win + 32) held one per lane
+      int32_t win = -64, lut_reg = 0;
+      auto blk = [&](int32_t j) -> int32_t {
+        if (!p.blk_ptr) return j;
+        const int32_t w = j & ~31;
+        if (w != win) {
+          win = w;
+          lut_reg = (w + lane < cnt) ? p.blk_idx[beg + w + lane] : 0;
         }
+        return __shfl_sync(0xffffffffu, lut_reg, j & 31);
+      };
+      // consumption order of the MMA warp (QK runs two blocks ahead of PV):
+      // K0, K1, K2, V0, K3, V1, ..., K_{n-1}, V_{n-3}, V_{n-2}, V_{n-1}
+      if (cnt > 0) load_tile(&tm_k, h, int64_t(blk(0)) * kBN);
+      if (cnt > 1) load_tile(&tm_k, h, int64_t(blk(1)) * kBN);
+      for (int32_t j = 0; j < cnt; ++j) {
+        if (j + 2 < cnt) load_tile(&tm_k, h, int64_t(blk(j + 2)) * kBN);
+        load_tile(&tm_v, h, int64_t(blk(j)) * kBN);
       }
     }
   } else if (warp == 1) {
     // ================================ MMA issuer ================================
-    if (lane == 0) {
-      uint32_t q_phase = 0, ring = 0, s_iter = 0, pv_iter = 0;
-      const uint32_t q_base = smem_u32(sQ);
-      auto next_slot = [&](uint32_t& slot) {
-        slot = ring % C::kStages;
-        trace(p, 0, ring);
-        mbar_wait(&bars->kv_full[slot], (ring / C::kStages) & 1);
-        trace(p, 1, ring);
-        ++ring;
-      };
-      // Three S/P buffers: QK_{j+2} overwrites S[(j+2)%3], whose P_{j-1} was consumed by
-      // PV_{j-1}, issued earlier into the in-order tcgen05 pipe — so QK never waits for the
-      // softmax, and the tensor pipe always has the next QK queued behind each PV.
-      auto issue_qk = [&]() {
-        uint32_t slot;
-        next_slot(slot);
-        const uint32_t sb = s_iter % C::kSBufs;
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(sRing + slot * C::kTileBytes);
+    // Warp-uniform control flow, one elected lane issues. Descriptors are kept as
+    // 32-bit halves: per K step only the low word moves (one uniform add), which
+    // keeps the issue path to a handful of instructions per UMMA — this warp shares
+    // its scheduler with four softmax warps, so its instruction count sets the
+    // tensor pipe's feed rate.
+    uint32_t q_phase = 0, ring = 0, s_iter = 0, pv_iter = 0;
+    constexpr uint32_t kHiK = desc_sw128_hi(1024);  // K-major SW128: LBO 16 B (unused), SBO 1024 B
+    const uint32_t q_lo = desc_sw128_lo(smem_u32(sQ), 16);
+    const uint32_t ring_lo = desc_sw128_lo(smem_u32(sRing), 16);
+    const uint32_t ring_lo_v = desc_sw128_lo(smem_u32(sRing), C::kChunkBytes);  // V: MN-major, LBO = chunk
+    auto next_slot = [&]() -> uint32_t {
+      const uint32_t slot = ring % C::kStages;
+      trace(p, 0, ring);
+      mbar_wait(&bars->kv_full[slot], (ring / C::kStages) & 1);
+      trace(p, 1, ring);
+      ++ring;
+      return slot;
+    };
+    // Three S/P buffers: QK_{j+2} overwrites S[(j+2)%3], whose P_{j-1} was consumed by
+    // PV_{j-1}, issued earlier into the in-order tcgen05 pipe — so QK never waits for the
+    // softmax, and the tensor pipe always has the next QK queued behind each PV.
+    auto issue_qk = [&]() {
+      const uint32_t slot = next_slot();
+      const uint32_t sb = s_iter % C::kSBufs;
+      tc_fence_after();
+      const uint32_t k_lo = ring_lo + slot * (C::kTileBytes >> 4);
+      if (elect_one()) {
 #pragma unroll
         for (int s = 0; s < D / 16; ++s) {
-          const uint32_t off = (s >> 2) * C::kChunkBytes + (s & 3) * 32;
-          if (!(p.exp_mode & 1))
-            umma_f16(tmem + sb * 128, smem_desc_sw128(q_base + off, 16, 1024), smem_desc_sw128(k_base + off, 16, 1024),
-                     C::kIdescQK, s > 0);
+          const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
+          umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off, kHiK, C::kIdescQK, s > 0);
         }
         umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->s_full[sb]);
-        ++s_iter;
-      };
-      auto issue_pv = [&](bool first) {
-        uint32_t slot;
-        next_slot(slot);
-        trace(p, 2, pv_iter);
-        mbar_wait(&bars->p_full, pv_iter & 1);
-        trace(p, 3, pv_iter);
-        tc_fence_after();
-        const uint32_t v_base = smem_u32(sRing + slot * C::kTileBytes);
-        const uint32_t p_tmem = tmem + (pv_iter % C::kSBufs) * 128;  // P_j aliases S_j (bf16 pairs)
+      }
+      __syncwarp();
+      ++s_iter;
+    };
+    auto issue_pv = [&](bool first) {
+      const uint32_t slot = next_slot();
+      const uint32_t pb = pv_iter % C::kSBufs;
+      trace(p, 2, pv_iter);
+      mbar_wait(&bars->p_full[pb], (pv_iter / C::kSBufs) & 1);
+      trace(p, 3, pv_iter);
+      tc_fence_after();
+      const uint32_t v_lo = ring_lo_v + slot * (C::kTileBytes >> 4);
+      const uint32_t p_tmem = tmem + pb * 128;  // P_j aliases S_j (bf16 pairs)
+      if (elect_one()) {
 #pragma unroll
         for (int s = 0; s < kBN / 16; ++s)
-          if (!(p.exp_mode & 2))
-            umma_f16_ts(tmem + C::kOCol, p_tmem + s * 8, smem_desc_sw128(v_base + s * 16 * 128, C::kChunkBytes, 1024),
-                        C::kIdescPV, (!first || s > 0) ? 1u : 0u);
+          umma_ts(tmem + C::kOCol, p_tmem + s * 8, v_lo + ((s * 16 * 128) >> 4), kHiK, C::kIdescPV,
+                  (!first || s > 0) ? 1u : 0u);
         umma_commit(&bars->kv_empty[slot]);
-        umma_commit(&bars->o_done);
-        ++pv_iter;
+        umma_commit(&bars->o_done[pb]);
+      }
+      __syncwarp();
+      ++pv_iter;
+    };
+    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      int64_t h, u;
+      int32_t beg, cnt;
+      tile_list(p, tile, h, u, beg, cnt);
+      mbar_wait(&bars->q_full, q_phase);
+      q_phase ^= 1;
+      if (cnt > 0) issue_qk();
+      if (cnt > 1) issue_qk();
+      auto release_q = [&]() {  // Q smem free once the last QK read it
+        if (elect_one()) umma_commit(&bars->q_empty);
+        __syncwarp();
       };
-      for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-        int64_t h, u;
-        int32_t beg, cnt;
-        tile_list(p, tile, h, u, beg, cnt);
-        mbar_wait(&bars->q_full, q_phase);
-        q_phase ^= 1;
-        issue_qk();
-        if (cnt > 1) issue_qk();
-        if (cnt <= 2) umma_commit(&bars->q_empty);  // Q smem free once the last QK read it
-        for (int32_t j = 0; j < cnt; ++j) {
-          if (j + 2 < cnt) {
-            issue_qk();
-            if (j + 3 == cnt) umma_commit(&bars->q_empty);
-          }
-          issue_pv(j == 0);
+      if (cnt <= 2) release_q();
+      for (int32_t j = 0; j < cnt; ++j) {
+        if (j + 2 < cnt) {
+          issue_qk();
+          if (j + 3 == cnt) release_q();
         }
+        issue_pv(j == 0);
       }
     }
   } else {
@@ -256,16 +294,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 2) >> 2;                    // key columns [32*wg, 32*wg + 32)
     const int r = (warp & 3) * 32 + lane;              // query row within the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
-    uint32_t s_iter = 0, o_phase = 0;
+    uint32_t s_iter = 0;
     float* red_max = red;                              // [parity][kWG][kBM]
     float* red_sum = red + 2 * kWG * kBM;              // [kWG][kBM]
+    // PV number g (CTA-global block counter) completes phase (g / 3) & 1 of o_done[g % 3].
+    // Waiting on it by parity is safe: S_{g+1} (or S_g at the epilogue) being ready implies
+    // PV_{g-3} completed (in-order tcgen05 pipe, QK_{g+1} is issued after PV_{g-2}), so the
+    // barrier is never more than one phase behind the one waited for.
+    auto wait_pv = [&](uint32_t g) { mbar_wait(&bars->o_done[g % C::kSBufs], (g / C::kSBufs) & 1); };
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
       int64_t h, u;
       int32_t beg, cnt;
       tile_list(p, tile, h, u, beg, cnt);
       float m = -INFINITY;
       uint64_t lsum[2] = {0, 0};  // packed fp32x2 partial row sums (2 independent chains)
-      int32_t vb_next = block_at(p, beg, 0);
+      int32_t vb_next = cnt > 0 ? block_at(p, beg, 0) : 0;
       for (int32_t j = 0; j < cnt; ++j) {
         const int32_t vb = vb_next;
         if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);  // prefetch: keeps the LUT load off the critical path
@@ -277,21 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars->s_full[sb], s_phase);
         if (tr) trace(p, 5 + (wg & 1) * 4, s_iter);
         tc_fence_after();
-        const uint32_t s_addr = tmem + lane_addr + sb * 128 + wg * 32;
-        if (p.exp_mode & 4) {  // debug: S -> P plumbing only
-          ++s_iter;
-          if (j > 0) {
-            mbar_wait(&bars->o_done, o_phase);
-            o_phase ^= 1;
-          }
-          tc_fence_before();
-          mbar_arrive(&bars->p_full);
-          continue;
-        }
         uint32_t sv[32];
-        tmem_ld32(s_addr, sv);
+        tmem_ld32(tmem + lane_addr + sb * 128 + wg * 32, sv);
         tmem_wait_ld();
-        ++s_iter;
         // padded keys of a partial last block (attention.cpp:146-152); warp-uniform branch
         const int valid = int(min(int64_t(kBN), p.nk - int64_t(vb) * kBN)) - wg * 32;
         if (valid < 32) {
@@ -305,19 +336,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         red_par[wg * kBM + r] = mx;
         named_bar_sync(kBarMax, kSoftmaxThreads);      // every slice loaded S and published its max
-        if (tr) trace(p, 6 + (wg & 1) * 4, s_iter - 1);
+        if (tr) trace(p, 6 + (wg & 1) * 4, s_iter);
 #pragma unroll
         for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
         const float m_new = fmaxf(m, mx * p.scale_log2);
-        bool waited = false;
         // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
         // (the partner warps cover the same rows, so they decide identically)
         if (j == 0) {
           m = m_new;
         } else if (__any_sync(0xffffffffu, m_new - m > kRescaleThreshold)) {
-          mbar_wait(&bars->o_done, o_phase);            // PV_{j-1} complete: O stable
-          o_phase ^= 1;
-          waited = true;
+          wait_pv(s_iter - 1);                          // PV_{j-1} complete: O stable
           tc_fence_after();
           const float alpha = ex2(m - m_new);
           const uint64_t a2 = f2_pack(alpha, alpha);
@@ -341,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st16(o_addr, ov);
           }
         }
-        // p = 2^(s*scale - m): 3 of every 4 pairs on MUFU, 1 on the FMA pipe (balances the pipes)
+        // p = 2^(s*scale - m); every POLY-th pair on the FMA pipe (offloads MUFU)
         const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
         uint32_t pk[16];
 #pragma unroll
@@ -349,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float x0, x1;
           f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
           float p0, p1;
-          if ((i & 3) == 3) {
+          if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == POLY - 1) {
             p0 = ex2_poly(x0);
             p1 = ex2_poly(x1);
           } else {
@@ -362,13 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // P_j (bf16 pairs) over the first 64 columns of S[sb]: this slice's 32 keys -> 16 columns
         tmem_st16(tmem + lane_addr + sb * 128 + wg * 16, pk);
         tmem_wait_st();
-        if (j > 0 && !waited) {
-          mbar_wait(&bars->o_done, o_phase);            // keep o_done phases in lock-step
-          o_phase ^= 1;
-        }
         tc_fence_before();
-        if (tr) trace(p, 7 + (wg & 1) * 4, s_iter - 1);
-        mbar_arrive(&bars->p_full);
+        if (tr) trace(p, 7 + (wg & 1) * 4, s_iter);
+        mbar_arrive(&bars->p_full[sb]);
+        ++s_iter;
       }
       float l;
       {
@@ -378,8 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // epilogue: wait for the last PV, combine the slices' row sums, normalise,
       // scatter this slice's columns of the row to its raster slot
-      mbar_wait(&bars->o_done, o_phase);
-      o_phase ^= 1;
+      if (cnt > 0) wait_pv(s_iter - 1);
       tc_fence_after();
       red_sum[wg * kBM + r] = l;   // dedicated slots: the max slots may still be read by peers
       named_bar_sync(kBarMax, kSoftmaxThreads);
@@ -468,15 +492,36 @@ int make_map(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t 
   return DFS_OK;
 }
 
-template <int D>
-int launch(const dfs_attn_args& a, float scale, cudaStream_t stream, int layout_hint) {
+template <int D, int POLY>
+int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const Params& p,
+                  cudaStream_t stream) {
   using C = Cfg<D>;
+  int dev = 0;
+  DFS_CUDA_CHECK(cudaGetDevice(&dev));
+  static bool attr_set[64] = {};
+  if (dev < 64 && !attr_set[dev]) {
+    DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        C::kSmem));
+    attr_set[dev] = true;
+  }
+  const int64_t grid = p.tiles < kNumSMs ? p.tiles : kNumSMs;
+  attn_sm100_kernel<D, POLY><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
+  DFS_LAUNCH_CHECK("attn_sm100");
+  return DFS_OK;
+}
+
+// exp2 split between MUFU and the FMA-pipe polynomial: every POLY-th pair of a
+// thread's 32 logits goes to the polynomial (0 = all MUFU). DFS_ATTN_POLY
+// overrides the default for A/B measurements.
+constexpr int kDefaultPoly = 4;
+
+template <int D>
+int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_map(&mq, a.q, a.in_layout, a.nq, a.heads, D))) return rc;
   if ((rc = make_map(&mk, a.k, a.in_layout, a.nk, a.heads, D))) return rc;
   if ((rc = make_map(&mv, a.v, a.in_layout, a.nk, a.heads, D))) return rc;
-  (void)layout_hint;
   Params p;
   p.heads = a.heads;
   p.nq = a.nq;
@@ -492,18 +537,19 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream, int layout_
   p.scale_log2 = scale * 1.4426950408889634f;
   p.tiles = p.mq * a.heads;
   p.trace = nullptr;
+#ifdef DFS_ATTN_TRACE_BUILD
   const char* trace_path = getenv("DFS_ATTN_TRACE");
-  p.exp_mode = getenv("DFS_ATTN_EXP") ? atoi(getenv("DFS_ATTN_EXP")) : 0;
   if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 16 * 256 * sizeof(unsigned long long)));
   if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 16 * 256 * sizeof(unsigned long long), stream));
-  static bool attr_set = false;
-  if (!attr_set) {
-    DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr_set = true;
+#endif
+  static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly;
+  switch (poly) {
+    case 0: rc = launch_kernel<D, 0>(mq, mk, mv, p, stream); break;
+    case 8: rc = launch_kernel<D, 8>(mq, mk, mv, p, stream); break;
+    default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
   }
-  const int64_t grid = p.tiles < kNumSMs ? p.tiles : kNumSMs;
-  attn_sm100_kernel<D><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
-  DFS_LAUNCH_CHECK("attn_sm100");
+  if (rc) return rc;
+#ifdef DFS_ATTN_TRACE_BUILD
   if (p.trace) {
     unsigned long long host[16 * 256];
     DFS_CUDA_CHECK(cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream));
@@ -514,6 +560,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream, int layout_
     }
     cudaFree(p.trace);
   }
+#endif
   return DFS_OK;
 }
 
@@ -543,8 +590,8 @@ bool attn_sm100_supports(const dfs_attn_args& a) {
 }
 
 int sparse_attn_sm100(const dfs_attn_args& a, float scale, cudaStream_t stream) {
-  if (a.d == 128) return launch<128>(a, scale, stream, 0);
-  if (a.d == 64) return launch<64>(a, scale, stream, 0);
+  if (a.d == 128) return launch<128>(a, scale, stream);
+  if (a.d == 64) return launch<64>(a, scale, stream);
   return fail(DFS_E_UNSUPPORTED, "attn_sm100: d must be 64 or 128");
 }
 

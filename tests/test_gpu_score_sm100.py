@@ -97,8 +97,9 @@ def test_scorer_extreme_magnitudes():
     """Per-head power-of-two scaling keeps both fp16 halves normal for tiny and huge inputs."""
     rng = np.random.default_rng(1)
     for scale in (1e-6, 8.0):  # logits std ~6 at 8.0; fp32 logits lose 1e-4 beyond ~|l| > 200
-        q = [rng.standard_normal((2048, 64)).astype(np.float32) * scale]
-        k = [rng.standard_normal((2048, 64)).astype(np.float32) * scale]
+        # bf16-rounded: the device path takes bf16 activations, the oracle the same values upcast
+        q = [bf16_round(rng.standard_normal((2048, 64)).astype(np.float32) * scale)]
+        k = [bf16_round(rng.standard_normal((2048, 64)).astype(np.float32) * scale)]
         fast = gpu_scores(q, k, 128, 16)
         ref = ora.block_scores(q[0], k[0], 128, 16)
         assert np.abs(fast[0] - ref).max() / np.abs(ref).max() <= 1e-4, scale

@@ -10,7 +10,8 @@
 
 using namespace dfsgpu::sm100;
 
-__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int mode, int n_dim, unsigned long long* out,
+template <int mode, int n_dim>
+__global__ void __launch_bounds__(128, 1) mma_kernel(int iters, unsigned long long* out,
                                                        const __grid_constant__ CUtensorMap map, int tma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -42,8 +43,24 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, int mode, int n_
         if (mode == 0)
           umma_f16(tmem + (it & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024), idesc,
                    s > 0);
-        else
+        else if (mode == 1)
           umma_f16_ts(tmem + (it & 1) * 128, tmem + 384 + s * 8, smem_desc_sw128(b + off, 16, 1024), idesc, s > 0);
+        else if (mode == 2)  // two independent SS accumulation chains, interleaved
+          umma_f16(tmem + (s & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024), idesc,
+                   s > 1);
+        else if (mode == 3) {  // K5 pattern: SS (QK into S) interleaved with TS (PV into O)
+          if (s & 1)
+            umma_f16_ts(tmem + 256, tmem + 384 + s * 8, smem_desc_sw128(b + off, 16, 1024), idesc, s > 1);
+          else
+            umma_f16(tmem + (it & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024),
+                     idesc, s > 1);
+        } else {  // mode 4: 8 SS into S then 8 TS into O (current K5 issue order), per pair of its
+          if (it & 1)
+            umma_f16_ts(tmem + 256, tmem + 384 + s * 8, smem_desc_sw128(b + off, 16, 1024), idesc, s > 0);
+          else
+            umma_f16(tmem + 128 * ((it >> 1) & 1), smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024),
+                     idesc, s > 0);
+        }
       }
     }
     umma_commit(&bar);
@@ -72,6 +89,23 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+using KFn = void (*)(int, unsigned long long*, const CUtensorMap, int);
+template <int M>
+KFn pick_n(int n) {
+  if (n == 64) return mma_kernel<M, 64>;
+  if (n == 128) return mma_kernel<M, 128>;
+  return mma_kernel<M, 256>;
+}
+KFn pick(int mode, int n) {
+  switch (mode) {
+    case 0: return pick_n<0>(n);
+    case 1: return pick_n<1>(n);
+    case 2: return pick_n<2>(n);
+    case 3: return pick_n<3>(n);
+    default: return pick_n<4>(n);
+  }
+}
+
 int main() {
   void* ptr = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -90,17 +124,19 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
   const int smem = 65536 + 65536 + 1024;
-  cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4000;
-  for (int mode = 0; mode < 2; ++mode)
-    for (int n : {128, 256})
-      for (int tma : {0, 2000, 6000}) {
+  for (int mode = 0; mode < 5; ++mode)
+    for (int n : {64, 128, 256})
+      for (int tma : {0}) {
+        if (n == 256 && mode >= 2) continue;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
-        mma_kernel<<<148, 128, smem>>>(iters, mode, n, d, map, tma);
+        auto kern = pick(mode, n);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<148, 128, smem>>>(iters, d, map, tma);
         cudaEventRecord(e0);
-        mma_kernel<<<148, 128, smem>>>(iters, mode, n, d, map, tma);
+        kern<<<148, 128, smem>>>(iters, d, map, tma);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -108,7 +144,7 @@ int main() {
         unsigned long long c[148];
         cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
         const double flops = 2.0 * 128 * n * 16 * 8.0 * iters * 148;
-        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", mode ? "TS" : "SS", n, tma,
+        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8"}[mode], n, tma,
                double(c[0]) / (iters * 8), ms, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
