@@ -35,7 +35,9 @@ using namespace sm100;
 
 constexpr int kRows = 128;
 constexpr int kKeys = 128;
-constexpr int kThreads = 192;
+constexpr int kSWG = 4;                   // softmax warpgroups: 32 key columns of each tile apiece
+constexpr int kSoftThreads = 128 * kSWG;
+constexpr int kThreads = 64 + kSoftThreads;
 constexpr float kLoScale = 2048.f;        // 2^11
 constexpr float kInvLoScale = 1.f / 2048.f;
 
@@ -47,7 +49,8 @@ struct SCfg {
   static constexpr int kStages = D == 64 ? 4 : 2;
   static constexpr int kQOff = 0;                         // Qhi, Qlo
   static constexpr int kKOff = 2 * kOpBytes;              // stages x (Khi, Klo)
-  static constexpr int kBarOff = kKOff + kStages * 2 * kOpBytes;
+  static constexpr int kRedOff = kKOff + kStages * 2 * kOpBytes;  // float m[kSWG][128], z[kSWG][128]
+  static constexpr int kBarOff = kRedOff + 2 * kSWG * kRows * 4;
   static constexpr int kSmem = kBarOff + 256 + 1024;
 };
 
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->acc_full[i], 1);
-      mbar_init(&bars->acc_free[i], 128);
+      mbar_init(&bars->acc_free[i], kSoftThreads);
     }
     fence_barrier_init();
   }
@@ -154,8 +157,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
+    // kSWG warpgroups split each 128-key tile by columns (32 apiece); a thread owns one
+    // pooled query row (TMEM lane) of its slice. Pass 0 keeps a per-slice online (max,
+    // sum), merged across the slices through shared memory once per row stripe.
+    const int wg = (warp - 2) >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
+    float* red_m = reinterpret_cast<float*>(smem + C::kRedOff);
+    float* red_z = red_m + kSWG * kRows;
     uint32_t acc_iter = 0;
     for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
       const int h = int(it / p.nrt), rt = int(it % p.nrt);
@@ -168,53 +177,70 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b = acc_iter & 1;
           mbar_wait(&bars->acc_full[b], (acc_iter >> 1) & 1);
           tc_fence_after();
-          const int64_t col0 = int64_t(kt) * kKeys;
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t a1[32], a2[32];
-            tmem_ld32(tmem + lane_addr + b * 256 + c * 32, a1);
-            tmem_ld32(tmem + lane_addr + b * 256 + 128 + c * 32, a2);
+          const int64_t cbase = int64_t(kt) * kKeys + wg * 32;
+          float l[32];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t a1[16], a2[16];
+            tmem_ld16(tmem + lane_addr + b * 256 + wg * 32 + c * 16, a1);
+            tmem_ld16(tmem + lane_addr + b * 256 + 128 + wg * 32 + c * 16, a2);
             tmem_wait_ld();
-            if (c == 3) {
-              tc_fence_before();
-              mbar_arrive(&bars->acc_free[b]);
-            }
-            float l[32];
-            const int64_t cbase = col0 + c * 32;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < 16; ++i) {
               const float x = fmaf(__uint_as_float(a2[i]), kInvLoScale, __uint_as_float(a1[i])) * f;
-              l[i] = (cbase + i < p.kvalid) ? x : -INFINITY;
+              l[c * 16 + i] = (cbase + c * 16 + i < p.kvalid) ? x : -INFINITY;
             }
-            if (pass == 0) {
-              float mx = l[0];
+          }
+          tc_fence_before();
+          mbar_arrive(&bars->acc_free[b]);
+          if (pass == 0) {
+            float mx = l[0];
 #pragma unroll
-              for (int i = 1; i < 32; ++i) mx = fmaxf(mx, l[i]);
-              const float mn = fmaxf(m, mx);
-              if (mn > -INFINITY) {
-                float s = 0.f;
+            for (int i = 1; i < 32; ++i) mx = fmaxf(mx, l[i]);
+            const float mn = fmaxf(m, mx);
+            if (mn > -INFINITY) {
+              float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) s += ex2(l[i] - mn);
-                z = z * ex2(m - mn) + s;
-                m = mn;
+              for (int i = 0; i < 32; i += 2) {
+                s0 += ex2(l[i] - mn);
+                s1 += ex2(l[i + 1] - mn);
               }
-            } else {
-              // probabilities (fp32, attention.cpp:120), summed over SUBS columns, then SUBS rows
+              z = z * ex2(m - mn) + (s0 + s1);
+              m = mn;
+            }
+          } else {
+            // probabilities (fp32, attention.cpp:120), summed over SUBS columns, then SUBS rows
 #pragma unroll
-              for (int g = 0; g < 32 / SUBS; ++g) {
-                float t = 0.f;
+            for (int g = 0; g < 32 / SUBS; ++g) {
+              float t = 0.f;
 #pragma unroll
-                for (int i = 0; i < SUBS; ++i) t += ex2(l[g * SUBS + i] - m) * inv_z;
+              for (int i = 0; i < SUBS; ++i) t += ex2(l[g * SUBS + i] - m) * inv_z;
 #pragma unroll
-                for (int o = 1; o < SUBS; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                const int64_t v = (cbase + g * SUBS) / SUBS;
-                if ((lane % SUBS) == 0 && u < p.m && v < p.m) p.S[(int64_t(h) * p.m + u) * p.m + v] = double(t);
-              }
+              for (int o = 1; o < SUBS; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+              const int64_t v = (cbase + g * SUBS) / SUBS;
+              if ((lane % SUBS) == 0 && u < p.m && v < p.m) p.S[(int64_t(h) * p.m + u) * p.m + v] = double(t);
             }
           }
           ++acc_iter;
         }
-        if (pass == 0) inv_z = 1.f / z;
+        if (pass == 0) {
+          // merge the slices' (max, sum) of this row
+          red_m[wg * kRows + r] = m;
+          red_z[wg * kRows + r] = z;
+          named_bar_sync(1, kSoftThreads);
+          float mm = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < kSWG; ++w) mm = fmaxf(mm, red_m[w * kRows + r]);
+          float zz = 0.f;
+#pragma unroll
+          for (int w = 0; w < kSWG; ++w) {
+            const float mw = red_m[w * kRows + r];
+            if (mw > -INFINITY) zz += red_z[w * kRows + r] * ex2(mw - mm);
+          }
+          named_bar_sync(1, kSoftThreads);  // slots are rewritten by the next stripe
+          m = mm;
+          inv_z = 1.f / zz;
+        }
       }
     }
   }

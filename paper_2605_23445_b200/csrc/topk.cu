@@ -119,6 +119,78 @@ __global__ void __launch_bounds__(kThreads) topk_kernel(const double* __restrict
   }
 }
 
+
+// ---- warp-per-row path (M <= 32 * CH): keys live in registers ------------------
+// Lane l holds the keys of blocks l, l + 32, ..., so a 32-wide chunk is one
+// coalesced row segment and a ballot over a chunk is in index order. The K-th
+// largest key T is found by bisection over the 64 key bits (MSB first), with an
+// early exit as soon as exactly K keys lie at or above the probe (then the
+// selection is those keys and no tie rule applies). Compaction: a ballot per
+// chunk gives each selected block its ascending slot.
+template <int CH>
+__global__ void __launch_bounds__(128) topk_warp_kernel(const double* __restrict__ scores, int64_t rows, int m, int k,
+                                                        int32_t* __restrict__ lut, uint8_t* __restrict__ sel) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const double* srow = scores + row * m;
+  uint64_t key[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = c * 32 + lane;
+    key[c] = i < m ? order_key(srow[i]) : 0ull;  // padding sorts below every real key (real keys have bit 63 set
+                                                 // or are ~b of a negative double, never 0 for finite input)
+  }
+  auto count_ge = [&](uint64_t t) {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) c += key[j] >= t;
+    return __reduce_add_sync(0xffffffffu, c);
+  };
+  // largest T with count(key >= T) >= k; stop early once count == k at the probe
+  uint64_t T = 0;
+  bool exact = false;
+  for (int bit = 63; bit >= 0; --bit) {
+    const uint64_t cand = T | (uint64_t(1) << bit);
+    const int c = count_ge(cand);
+    if (c >= k) {
+      T = cand;
+      if (c == k) {
+        exact = true;
+        break;
+      }
+    }
+  }
+  int need_eq = k;  // keys equal to T taken, lowest indices first (stable-sort tie rule)
+  if (!exact) {
+    int gt = 0;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) gt += key[j] > T;
+    need_eq = k - __reduce_add_sync(0xffffffffu, gt);
+  }
+  int32_t* lrow = lut ? lut + row * k : nullptr;
+  uint8_t* brow = sel ? sel + row * m : nullptr;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  int pos = 0, eq_seen = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int i = c * 32 + lane;
+    bool take;
+    if (exact) {
+      take = i < m && key[c] >= T;
+    } else {
+      const bool eq = i < m && key[c] == T;
+      const uint32_t eqb = __ballot_sync(0xffffffffu, eq);
+      take = (i < m && key[c] > T) || (eq && eq_seen + __popc(eqb & lt_mask) < need_eq);
+      eq_seen += __popc(eqb);
+    }
+    const uint32_t tb = __ballot_sync(0xffffffffu, take);
+    if (take && lrow) lrow[pos + __popc(tb & lt_mask)] = i;
+    if (brow && i < m) brow[i] = take;
+    pos += __popc(tb);
+  }
+}
+
 // BlockMask payload: bit (u, v) at idx = u*M + v, MSB-first (block_mask.hpp:36-48)
 __global__ void pack_bits_kernel(const uint8_t* __restrict__ sel, int64_t m, int64_t bytes,
                                  uint8_t* __restrict__ bits) {
@@ -209,10 +281,18 @@ int topk_select_impl(const double* scores, int64_t heads, int64_t m, int64_t k, 
                      uint8_t* bits, cudaStream_t stream) {
   if (m < 1 || k < 1 || k > m) return fail(DFS_E_INVALID, "topk_select: need 1 <= K <= M");
   if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large for the smem kernel");
-  const size_t smem = size_t(m) * sizeof(uint64_t);
-  if (smem > 48 * 1024)
-    DFS_CUDA_CHECK(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  topk_kernel<<<unsigned(heads * m), kThreads, smem, stream>>>(scores, int(m), int(k), lut, sel);
+  const int64_t rows = heads * m;
+  const unsigned wgrid = unsigned(ceil_div(rows, 4));
+  if (m <= 32 * 8) {
+    topk_warp_kernel<8><<<wgrid, 128, 0, stream>>>(scores, rows, int(m), int(k), lut, sel);
+  } else if (m <= 32 * 32) {
+    topk_warp_kernel<32><<<wgrid, 128, 0, stream>>>(scores, rows, int(m), int(k), lut, sel);
+  } else {
+    const size_t smem = size_t(m) * sizeof(uint64_t);
+    if (smem > 48 * 1024)
+      DFS_CUDA_CHECK(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    topk_kernel<<<unsigned(rows), kThreads, smem, stream>>>(scores, int(m), int(k), lut, sel);
+  }
   DFS_LAUNCH_CHECK("topk_select");
   if (bits) {
     const int64_t bytes = (m * m + 7) / 8;

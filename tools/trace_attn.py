@@ -1,3 +1,4 @@
+"""Per-block timeline of one CTA of K5 at HY (needs a -DDFS_ATTN_TRACE_BUILD library via DFS_B200_LIB)."""
 import os, sys, numpy as np, torch
 sys.path.insert(0, '.')
 os.environ['DFS_ATTN_TRACE'] = 'gpurun_out/attn_trace.bin'
@@ -5,7 +6,7 @@ import paper_2605_23445_b200 as m
 from paper_2605_23445_b200 import ops
 from bench import smooth_fields
 dims, H, d = (33, 45, 80), 24, 128
-n = 33*45*80
+n = 33 * 45 * 80
 q, k, v = smooth_fields(dims, H, d, 1, torch.device('cuda'))
 perm = m.hilbert3d_order(dims)
 qh, pq = ops.permute_to_hnd(q, perm, 16); kh, pk = ops.permute_to_hnd(k, perm, 16); vh, _ = ops.permute_to_hnd(v, perm, 0)
@@ -13,11 +14,18 @@ S = ops.score_pooled(pq, pk, n, m.ScoringParams(128, 16)); lut = m.topk_lut(S, 0
 os.makedirs('gpurun_out', exist_ok=True)
 o = m.sparse_attention_csr(qh, kh, vh, ptr, lut.reshape(-1), 128); torch.cuda.synchronize()
 t = np.fromfile('gpurun_out/attn_trace.bin', dtype=np.uint64).reshape(16, 256).astype(np.int64)
-t0 = t[t > 0].min()
-names = ['kv_wait_start', 'kv_wait_done', 'p_wait_start', 'p_wait_done', 'wg0_s_wait', 'wg0_s_ready', 'wg0_barrier', 'wg0_arrive', 'wg1_s_wait', 'wg1_s_ready', 'wg1_barrier', 'wg1_arrive']
+names = ['kv_wait_start', 'kv_wait_done', 'p_wait_start', 'p_wait_done', 'A_s_wait', 'A_s_ready', 'A_barrier',
+         'A_arrive', 'B_s_wait', 'B_s_ready', 'B_barrier', 'B_arrive']
+lo, hi = 60, 120
+t0 = t[0, lo * 2]
 for i, nm in enumerate(names):
-    row = t[i] - t0
-    print(f"{nm:14s}", ' '.join(f"{x:7d}" for x in row[100:112]))
-sr = t[5, 100:200] - t[4, 100:200]; ar = t[7, 100:200] - t[5, 100:200]; pw = t[3, 100:200] - t[2, 100:200]
-print('per-block period wg0 arrive', np.diff(t[7, 100:200]).mean(), 'softmax busy', ar.mean(), 's_full wait', sr.mean(), 'MMA p_full wait', pw.mean())
-print('kv wait', (t[1, 100:200] - t[0, 100:200]).mean())
+    print(f"{nm:14s}", ' '.join(f"{x - t0:7d}" for x in t[i, lo:lo + 12]))
+for s, base in (("A", 4), ("B", 8)):
+    w = (t[base + 1, lo:hi] - t[base, lo:hi]).mean()
+    busy = (t[base + 3, lo:hi] - t[base + 1, lo:hi]).mean()
+    pre = (t[base + 2, lo:hi] - t[base + 1, lo:hi]).mean()
+    per = np.diff(t[base + 3, lo:hi]).mean()
+    print(f"stream {s}: period/block {per:.0f} (2 blocks of the tile), S wait {w:.0f}, busy {busy:.0f} (to barrier {pre:.0f})")
+pw = (t[3, lo:hi] - t[2, lo:hi]).mean()
+kvw = (t[1, 2 * lo:2 * hi] - t[0, 2 * lo:2 * hi]).mean()
+print(f"MMA: p_full wait/PV {pw:.0f}, kv wait/ring entry {kvw:.0f}, PV period {np.diff(t[2, lo:hi]).mean():.0f}")
