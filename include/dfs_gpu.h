@@ -145,6 +145,7 @@ typedef struct {
   const uint32_t* out_rows;
   float scale;
   int force_generic; /* 1: use the SIMT kernel even when the tcgen05 one applies */
+  int64_t dv;        /* head dim of v / o; 0 = d (dv != d: fp32 kernel only) */
 } dfs_attn_args;
 int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream);
 
@@ -205,6 +206,34 @@ typedef struct {
   double* sparsity_out;  /* [H] realized sparsity per head (metrics.cpp:39) */
 } dfs_step_args;
 int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
+
+/* ============ Matrix-level companions used by the dfs:: drop-in shim =========== */
+/* attention.cpp:105-123 attention_scores (and the pooled softmax inside
+ * mask_builder.cpp:30-62 subblock_scores): row-softmax(q k^T * scale) with fp64
+ * logits/exp/sum, fp32 probabilities. q [H, q_valid, d], k [H, k_valid, d] fp32
+ * device; probs [H, q_rows, k_cols]. Rows >= q_valid are zero vectors (uniform
+ * over the valid keys), columns >= k_valid are 0. scale <= 0 means 1/sqrt(d). */
+int dfs_softmax_scores(const float* q, const float* k, int64_t heads, int64_t q_valid, int64_t q_rows,
+                       int64_t k_valid, int64_t k_cols, int64_t d, double scale, float* probs,
+                       dfs_stream stream);
+/* mask_builder.cpp:64-80 aggregate_scores: S [H, mq, mk] fp64 tile sums of
+ * probs [H, mq*subs, mk*subs]. */
+int dfs_aggregate_scores(const float* probs, int64_t heads, int64_t mq, int64_t mk, int64_t subs,
+                         double* scores, dfs_stream stream);
+/* mask_builder.cpp:91-102 top_indices for `rows` independent rows of length n:
+ * out [rows, k] ascending indices of the k best (value desc, index asc). */
+int dfs_top_indices(const double* values, int64_t rows, int64_t n, int64_t k, int32_t* out,
+                    dfs_stream stream);
+/* attention.cpp:161-173 masked_scores (scores [rows, cols] fp32, BlockMask
+ * payload bits of an m x m mask with block size `block`). */
+int dfs_masked_scores(const float* scores, int64_t rows, int64_t cols, const uint8_t* bits, int64_t m,
+                      int64_t block, float* out, dfs_stream stream);
+/* attention.cpp:19-20 (non-finite input is an error): *nonfinite_host = 1 when
+ * any of `count` elements (dtype) is NaN/Inf. Synchronises the stream. */
+int dfs_check_finite(const void* x, int64_t count, int dtype, int* nonfinite_host, dfs_stream stream);
+/* attention.cpp:175-190 attention_recall -> *recall_host (synchronises). */
+int dfs_attention_recall(const float* scores, int64_t rows, int64_t cols, const uint8_t* bits, int64_t m,
+                         int64_t block, double* recall_host, dfs_stream stream);
 
 /* Per-handle kernel selection (A/B tests): route scoring / attention through
  * the geometry-generic kernels even where the tcgen05 ones apply. */

@@ -39,7 +39,7 @@ class AttnArgs(C.Structure):
     _fields_ = [("q", _p), ("k", _p), ("v", _p), ("o", _p), ("dtype", _i32), ("in_layout", _i32),
                 ("out_layout", _i32), ("heads", _i64), ("nq", _i64), ("nk", _i64), ("d", _i64),
                 ("block", _i64), ("blk_ptr", _p), ("blk_idx", _p), ("out_rows", _p), ("scale", _f),
-                ("force_generic", _i32)]
+                ("force_generic", _i32), ("dv", _i64)]
 
 
 class Schedule(C.Structure):
@@ -82,6 +82,12 @@ _SIGS = {
     "dfs_mask_cache_store": (_i32, [_p, _i32, _i32, _p, _i64, _i64, _i32, _p]),
     "dfs_mask_cache_size": (_i32, [_p, C.POINTER(_i64)]),
     "dfs_run_step": (_i32, [_p, C.POINTER(Schedule), C.POINTER(StepArgs), _p]),
+    "dfs_softmax_scores": (_i32, [_p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _dbl, _p, _p]),
+    "dfs_aggregate_scores": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p]),
+    "dfs_top_indices": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
+    "dfs_masked_scores": (_i32, [_p, _i64, _i64, _p, _i64, _i64, _p, _p]),
+    "dfs_check_finite": (_i32, [_p, _i64, _i32, C.POINTER(_i32), _p]),
+    "dfs_attention_recall": (_i32, [_p, _i64, _i64, _p, _i64, _i64, C.POINTER(_dbl), _p]),
 }
 
 EXPORTS = tuple(_SIGS)

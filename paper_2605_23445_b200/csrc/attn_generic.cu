@@ -113,12 +113,110 @@ int dispatch_d(const dfs_attn_args& a, int64_t mq, float scale, cudaStream_t str
   return fail(DFS_E_UNSUPPORTED, "sparse_attn: d > 256");
 }
 
+
+// ---- fp32 drop-in path: the reference's fp64 arithmetic -------------------------
+// For DFS_F32 inputs (the dfs::Matrix API) the softmax and the weighted sum run in
+// fp64 like attend_row (attention.cpp:32-60): one warp per query row, lanes split
+// the head dim (DPL = d/32 rounded up values each), every logit is a warp-reduced
+// fp64 dot product. Pass 1 keeps an online (max, sum); pass 2 recomputes each
+// logit, forms p = exp(l - max) / z and accumulates p * v in fp64; the result is
+// rounded to fp32 once, as the reference does. Keys come from the CSR block list
+// in ascending order and are clipped to nk.
+template <int DPL>
+__global__ void __launch_bounds__(128) attn_f64_kernel(dfs_attn_args a, int64_t mq, double scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  const int64_t h = blockIdx.y;
+  if (row >= a.nq) return;
+  const int64_t d = a.d, dv = a.dv > 0 ? a.dv : a.d, B = a.block, u = row / B;
+  const float* q = static_cast<const float*>(a.q);
+  const float* k = static_cast<const float*>(a.k);
+  const float* v = static_cast<const float*>(a.v);
+  const int64_t mk = ceil_div(a.nk, B);
+  const int32_t beg = a.blk_ptr ? a.blk_ptr[h * mq + u] : 0;
+  const int32_t end = a.blk_ptr ? a.blk_ptr[h * mq + u + 1] : int32_t(mk);
+  double qv[DPL];
+  const float* qrow = q + row_offset(a.in_layout, a.nq, a.heads, d, h, row);
+#pragma unroll
+  for (int t = 0; t < DPL; ++t) {
+    const int64_t c = lane + 32 * t;
+    qv[t] = c < d ? double(qrow[c]) : 0.0;
+  }
+  auto logit = [&](int64_t j) {
+    const float* krow = k + row_offset(a.in_layout, a.nk, a.heads, d, h, j);
+    double acc = 0.0;
+#pragma unroll
+    for (int t = 0; t < DPL; ++t) {
+      const int64_t c = lane + 32 * t;
+      if (c < d) acc += qv[t] * double(krow[c]);
+    }
+    return warp_sum_d(acc) * scale;
+  };
+  double mx = -INFINITY, z = 0.0;
+  for (int32_t e = beg; e < end; ++e) {
+    const int64_t vb = a.blk_idx ? a.blk_idx[e] : e;
+    const int64_t hi = min((vb + 1) * B, a.nk);
+    for (int64_t j = vb * B; j < hi; ++j) {
+      const double l = logit(j);
+      if (l > mx) {
+        z = z * exp(mx - l);
+        mx = l;
+      }
+      z += exp(l - mx);
+    }
+  }
+  double acc[DPL];
+#pragma unroll
+  for (int t = 0; t < DPL; ++t) acc[t] = 0.0;
+  for (int32_t e = beg; e < end; ++e) {
+    const int64_t vb = a.blk_idx ? a.blk_idx[e] : e;
+    const int64_t hi = min((vb + 1) * B, a.nk);
+    for (int64_t j = vb * B; j < hi; ++j) {
+      const double p = exp(logit(j) - mx) / z;
+      const float* vrow = v + row_offset(a.in_layout, a.nk, a.heads, dv, h, j);
+#pragma unroll
+      for (int t = 0; t < DPL; ++t) {
+        const int64_t c = lane + 32 * t;
+        if (c < dv) acc[t] += p * double(vrow[c]);
+      }
+    }
+  }
+  const int64_t orow = a.out_rows ? int64_t(a.out_rows[row]) : row;
+  float* dst = static_cast<float*>(a.o) + row_offset(a.out_layout, a.nq, a.heads, dv, h, orow);
+#pragma unroll
+  for (int t = 0; t < DPL; ++t) {
+    const int64_t c = lane + 32 * t;
+    if (c < dv) dst[c] = float(acc[t]);
+  }
+}
+
+template <int DPL>
+int launch_f64(const dfs_attn_args& a, int64_t mq, double scale, cudaStream_t stream) {
+  dim3 grid(unsigned(ceil_div(a.nq, 4)), unsigned(a.heads));
+  attn_f64_kernel<DPL><<<grid, 128, 0, stream>>>(a, mq, scale);
+  DFS_LAUNCH_CHECK("sparse_attn_f64");
+  return DFS_OK;
+}
+
 }  // namespace
 
 int sparse_attn_generic(const dfs_attn_args& a, float scale, cudaStream_t stream) {
+  if (a.dv > 0 && a.dv != a.d && a.dtype != DFS_F32)
+    return fail(DFS_E_UNSUPPORTED, "sparse_attn: dv != d only on the fp32 path");
   const int64_t mq = ceil_div(a.nq, a.block);
   if (mq > 2147483647LL || a.heads > 65535) return fail(DFS_E_UNSUPPORTED, "sparse_attn: grid too large");
-  if (a.dtype == DFS_F32) return dispatch_d<float>(a, mq, scale, stream);
+  if (a.dtype == DFS_F32) {
+    // fp64 softmax and accumulation (the reference's arithmetic); the scale is recomputed
+    // in fp64 when the caller asked for the default 1/sqrt(d)
+    const double sc = a.scale > 0.f ? double(a.scale) : 1.0 / sqrt(double(a.d));
+    if (a.heads > 65535 || ceil_div(a.nq, 4) > 2147483647LL) return fail(DFS_E_UNSUPPORTED, "sparse_attn: grid too large");
+    const int64_t dmax = a.dv > a.d ? a.dv : a.d;
+    if (dmax <= 32) return launch_f64<1>(a, mq, sc, stream);
+    if (dmax <= 64) return launch_f64<2>(a, mq, sc, stream);
+    if (dmax <= 128) return launch_f64<4>(a, mq, sc, stream);
+    if (dmax <= 256) return launch_f64<8>(a, mq, sc, stream);
+    return fail(DFS_E_UNSUPPORTED, "sparse_attn: d > 256");
+  }
   if (a.dtype == DFS_BF16) return dispatch_d<__nv_bfloat16>(a, mq, scale, stream);
   return fail(DFS_E_INVALID, "sparse_attn: unknown dtype");
 }

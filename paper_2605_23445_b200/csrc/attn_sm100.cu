@@ -582,6 +582,7 @@ int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads
 
 bool attn_sm100_supports(const dfs_attn_args& a) {
   if (a.dtype != DFS_BF16 || a.block != 128 || (a.d != 64 && a.d != 128)) return false;
+  if (a.dv > 0 && a.dv != a.d) return false;
   const void* ptrs[4] = {a.q, a.k, a.v, a.o};
   for (const void* ptr : ptrs)
     if (reinterpret_cast<uintptr_t>(ptr) & 15) return false;

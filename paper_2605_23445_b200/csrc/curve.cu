@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kThreads) write_kernel(Geometry g, const int* 
 
 __global__ void invert_kernel(const uint32_t* __restrict__ fwd, int64_t n, uint32_t* __restrict__ inv) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    inv[fwd[i]] = uint32_t(i);
+    if (int64_t(fwd[i]) < n) inv[fwd[i]] = uint32_t(i);  // out-of-range entries: no wild write
 }
 
 __global__ void histogram_kernel(const uint32_t* __restrict__ fwd, int64_t n, int* __restrict__ seen,

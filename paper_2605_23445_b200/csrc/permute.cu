@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ src,
       // gather: read source row idx[i] -> write dest row i; scatter: the reverse
       const int64_t si = kScatter ? i : int64_t(idx[i]);
       const int64_t di = kScatter ? int64_t(idx[i]) : i;
+      if (si >= n || di >= n) continue;  // invalid permutation entry: no wild access
       const uint4 u = *reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c);
       *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) = u;
       if (kPool || nonfinite) {
@@ -116,6 +117,7 @@ __global__ void permute_scalar_kernel(const T* __restrict__ src, int src_layout,
       if (i >= n) break;
       const int64_t si = kScatter ? i : int64_t(idx[i]);
       const int64_t di = kScatter ? int64_t(idx[i]) : i;
+      if (si >= n || di >= n) continue;
       const T x = src[row_offset(src_layout, n, heads, d, h, si) + c];
       dst[row_offset(dst_layout, n, heads, d, h, di) + c] = x;
       const float xf = to_f32<T>(x);

@@ -94,17 +94,20 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restri
   }
 }
 
-__global__ void aggregate_kernel(const float* __restrict__ P, int64_t m, int64_t subs, int64_t kcols,
-                                 int64_t qrows, double* __restrict__ S) {
+// S[u][v] = sum of the subs x subs tile (u, v) of P, fp64 in the reference's (i, j)
+// order (mask_builder.cpp:64-80); mq x mk blocks, P is [mq*subs, mk*subs] per head.
+__global__ void aggregate_kernel(const float* __restrict__ P, int64_t mq, int64_t mk, int64_t subs,
+                                 double* __restrict__ S) {
   const int64_t h = blockIdx.y;
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= m * m) return;
-  const int64_t u = t / m, v = t % m;
-  const float* p = P + h * qrows * kcols;
+  if (t >= mq * mk) return;
+  const int64_t u = t / mk, v = t % mk;
+  const int64_t kcols = mk * subs;
+  const float* p = P + h * mq * subs * kcols;
   double acc = 0.0;
   for (int64_t i = u * subs; i < (u + 1) * subs; ++i)
     for (int64_t j = v * subs; j < (v + 1) * subs; ++j) acc += double(p[i * kcols + j]);
-  S[h * m * m + t] = acc;
+  S[h * mq * mk + t] = acc;
 }
 
 }  // namespace
@@ -134,26 +137,36 @@ int score_blocks_generic(const float* pq, const float* pk, int64_t heads, int64_
     softmax_rows_kernel<<<g1, 256, smem, stream>>>(pq + h0 * valid * d, pk + h0 * valid * d, valid, qrows, valid,
                                                    kcols, d, scale, P_ws);
     dim3 g2(unsigned(ceil_div(m * m, 256)), unsigned(hb));
-    aggregate_kernel<<<g2, 256, 0, stream>>>(P_ws, m, subs, kcols, qrows, S + h0 * m * m);
+    aggregate_kernel<<<g2, 256, 0, stream>>>(P_ws, m, m, subs, S + h0 * m * m);
     DFS_LAUNCH_CHECK("score_blocks_generic");
   }
   return DFS_OK;
 }
 
-// the fp32 sub-block probability matrix alone (mask_builder.hpp:221 subblock_scores)
-int subblock_scores_generic(const float* pq, const float* pk, int64_t n, int64_t d, int64_t block,
-                            int64_t sub_block, float* P, cudaStream_t stream) {
-  if (d > 256) return fail(DFS_E_UNSUPPORTED, "subblock_scores: generic path needs d <= 256");
-  const int64_t subs = block / sub_block;
-  const int64_t qrows = ceil_div(n, block) * subs;
-  const int64_t valid = ceil_div(n, sub_block);
+// Row softmax of q k^T * scale (attention.cpp:105-123 attention_scores, and the
+// pooled form inside subblock_scores, mask_builder.cpp:30-62): q [H, qvalid, d],
+// k [H, kvalid, d] fp32 -> P [H, qrows, kcols] fp32 with fp64 logits/exp/sum.
+// Rows >= qvalid are zero vectors (uniform over the valid keys), columns >= kvalid
+// stay 0.
+int softmax_scores_impl(const float* q, const float* k, int64_t heads, int64_t qvalid, int64_t qrows,
+                        int64_t kvalid, int64_t kcols, int64_t d, double scale, float* P, cudaStream_t stream) {
+  if (d > 256) return fail(DFS_E_UNSUPPORTED, "attention_scores: d > 256");
+  if (heads > 65535) return fail(DFS_E_UNSUPPORTED, "attention_scores: too many heads");
   const size_t smem = size_t(2 * kRows * (d + 1)) * sizeof(float);
   if (smem > 48 * 1024)
     DFS_CUDA_CHECK(cudaFuncSetAttribute(softmax_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(smem)));
-  dim3 g1(unsigned(ceil_div(qrows, kRows)), 1);
-  softmax_rows_kernel<<<g1, 256, smem, stream>>>(pq, pk, valid, qrows, valid, qrows, d, 1.0 / sqrt(double(d)), P);
-  DFS_LAUNCH_CHECK("subblock_scores_generic");
+  dim3 g1(unsigned(ceil_div(qrows, kRows)), unsigned(heads));
+  softmax_rows_kernel<<<g1, 256, smem, stream>>>(q, k, qvalid, qrows, kvalid, kcols, d, scale, P);
+  DFS_LAUNCH_CHECK("softmax_scores");
+  return DFS_OK;
+}
+
+int aggregate_scores_impl(const float* P, int64_t heads, int64_t mq, int64_t mk, int64_t subs, double* S,
+                          cudaStream_t stream) {
+  dim3 g2(unsigned(ceil_div(mq * mk, 256)), unsigned(heads));
+  aggregate_kernel<<<g2, 256, 0, stream>>>(P, mq, mk, subs, S);
+  DFS_LAUNCH_CHECK("aggregate_scores");
   return DFS_OK;
 }
 

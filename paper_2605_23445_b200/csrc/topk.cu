@@ -277,23 +277,33 @@ __global__ void lut_ptr_kernel(int64_t rows, int64_t k, int32_t* __restrict__ pt
 
 int64_t topk_max_m() { return (200 * 1024) / 8; }
 
-int topk_select_impl(const double* scores, int64_t heads, int64_t m, int64_t k, int32_t* lut, uint8_t* sel,
-                     uint8_t* bits, cudaStream_t stream) {
-  if (m < 1 || k < 1 || k > m) return fail(DFS_E_INVALID, "topk_select: need 1 <= K <= M");
-  if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large for the smem kernel");
-  const int64_t rows = heads * m;
+// rows independent rows of length n: the k best (desc value, asc index), ascending
+// (mask_builder.cpp:91-102 top_indices); sel (optional) gets a 0/1 byte per element.
+int top_indices_impl(const double* values, int64_t rows, int64_t n, int64_t k, int32_t* out, uint8_t* sel,
+                     cudaStream_t stream) {
+  if (n < 1 || k < 1 || k > n) return fail(DFS_E_INVALID, "top_indices: need 1 <= k <= n");
+  if (n > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "top_indices: row too long for the smem kernel");
+  const int64_t m = n;
+  int32_t* lut = out;
   const unsigned wgrid = unsigned(ceil_div(rows, 4));
   if (m <= 32 * 8) {
-    topk_warp_kernel<8><<<wgrid, 128, 0, stream>>>(scores, rows, int(m), int(k), lut, sel);
+    topk_warp_kernel<8><<<wgrid, 128, 0, stream>>>(values, rows, int(m), int(k), lut, sel);
   } else if (m <= 32 * 32) {
-    topk_warp_kernel<32><<<wgrid, 128, 0, stream>>>(scores, rows, int(m), int(k), lut, sel);
+    topk_warp_kernel<32><<<wgrid, 128, 0, stream>>>(values, rows, int(m), int(k), lut, sel);
   } else {
     const size_t smem = size_t(m) * sizeof(uint64_t);
     if (smem > 48 * 1024)
       DFS_CUDA_CHECK(cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    topk_kernel<<<unsigned(rows), kThreads, smem, stream>>>(scores, int(m), int(k), lut, sel);
+    topk_kernel<<<unsigned(rows), kThreads, smem, stream>>>(values, int(m), int(k), lut, sel);
   }
   DFS_LAUNCH_CHECK("topk_select");
+  return DFS_OK;
+}
+
+int topk_select_impl(const double* scores, int64_t heads, int64_t m, int64_t k, int32_t* lut, uint8_t* sel,
+                     uint8_t* bits, cudaStream_t stream) {
+  if (m < 1 || k < 1 || k > m) return fail(DFS_E_INVALID, "topk_select: need 1 <= K <= M");
+  if (int rc = top_indices_impl(scores, heads * m, m, k, lut, sel, stream)) return rc;
   if (bits) {
     const int64_t bytes = (m * m + 7) / 8;
     dim3 g(unsigned(ceil_div(bytes, 256)), unsigned(heads));
