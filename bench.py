@@ -124,6 +124,25 @@ def smooth_fields(dims, heads, d, seed, device, rounds=4):
     return out
 
 
+def k5_traffic(workload, heads_local):
+    """DRAM bytes (read + write) per K5 launch from the committed ncu --set full capture
+    (profiles/<round>/k5_traffic.json), scaled to this rank's head count; None if absent."""
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "k5_traffic.json"))):
+        try:
+            with open(path) as f:
+                rec = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if rec.get("workload") == workload:
+            best = rec
+    if not best:
+        return None
+    return best["dram_bytes_per_launch"] * heads_local / best["heads"]
+
+
 def executed_flops(lut, n, block, d):
     """4*d*sum over (head, u, v in I_u) of r_u*c_v with real token counts."""
     import torch
@@ -235,6 +254,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-units-per-thread", type=int, default=20)
     ap.add_argument("--profile", action="store_true", help="only run warmup+steps of the step (for ncu)")
+    ap.add_argument("--ulysses", action="store_true",
+                    help="sequence-sharded inputs [N/P, H, d]: NCCL all-to-all to heads, step, all-to-all back "
+                         "(inside the timed region); default: head-sharded inputs, no collective")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -260,7 +282,19 @@ def main():
     m = -(-n // B)
     h0, h1 = rank * H // world, (rank + 1) * H // world
     hl = h1 - h0
-    q, k, v = smooth_fields(dims, hl, d, seed=1000 + rank, device=dev)
+    ulysses_mode = args.ulysses and world > 1
+    if ulysses_mode:
+        from paper_2605_23445_b200 import ulysses
+
+        if n % world or H % world:
+            raise SystemExit(f"--ulysses needs tokens and heads divisible by {world}")
+        nl = n // world
+        full = smooth_fields(dims, H, d, seed=1000, device=dev)  # same field on every rank; keep my token shard
+        ql, kl, vl = (x[rank * nl:(rank + 1) * nl].contiguous() for x in full)
+        del full
+        q, k, v = ulysses.seq_to_head([ql, kl, vl])  # head-local view, for the kernel breakdown only
+    else:
+        q, k, v = smooth_fields(dims, hl, d, seed=1000 + rank, device=dev)
     params = dfs.ScoringParams(B, Bs)
     sched = dfs.SparsitySchedule(total_steps=1, warmup_fraction=0.0, phase_budgets=(gamma,), phase_fraction=1.0,
                                  update_interval=1)
@@ -275,7 +309,10 @@ def main():
         torch.cuda.synchronize()
 
     def step():
-        dfs.run_step(q, k, v, dims, params, sched, cache, layer=0, step=0, out=out)
+        if ulysses_mode:
+            ulysses.ulysses_run_step(ql, kl, vl, dims, params, sched, cache, layer=0, step=0)
+        else:
+            dfs.run_step(q, k, v, dims, params, sched, cache, layer=0, step=0, out=out)
 
     for _ in range(args.warmup):
         step()
@@ -345,38 +382,66 @@ def main():
     attn_flops_local = executed_flops(lut, n, B, d)
     achieved = attn_flops_local / (t_attn * 1e-3) / 1e12
 
-    # ---- e2e: host buffers through the public API, copies inside the timed region
+    # ---- e2e: host buffers through the public API, copies inside the timed region.
+    # Every step copies its own inputs host->device (pinned) and its output back;
+    # two buffer sets and separate copy streams let step i+1's upload and step
+    # i-1's download overlap step i's kernels (PCIe is the bound, not the GPU).
     e2e = None
-    if rank == 0 or world > 1:
-        qh_, kh_, vh_ = (x.cpu().pin_memory() for x in (q, k, v))
-        oh_ = torch.empty_like(qh_).pin_memory()
-        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    src = (ql, kl, vl) if ulysses_mode else (q, k, v)
+    host_in = [tuple(x.cpu().pin_memory() for x in src) for _ in range(2)]
+    host_out = [torch.empty(src[0].shape, dtype=src[0].dtype).pin_memory() for _ in range(2)]
+    dev_in = [tuple(torch.empty_like(x) for x in src) for _ in range(2)]
+    dev_out = [torch.empty_like(src[0]) for _ in range(2)]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_done = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step():
-            qd.copy_(qh_, non_blocking=True)
-            kd.copy_(kh_, non_blocking=True)
-            vd.copy_(vh_, non_blocking=True)
-            dfs.run_step(qd, kd, vd, dims, params, sched, cache, layer=0, step=0, out=out)
-            oh_.copy_(out, non_blocking=True)
+    def e2e_step(i):
+        b = i % 2
+        with torch.cuda.stream(h2d_s):
+            h2d_s.wait_event(ev_done[b])  # step i-2 finished reading these device inputs
+            for x_d, x_h in zip(dev_in[b], host_in[b]):
+                x_d.copy_(x_h, non_blocking=True)
+            ev_in[b].record(h2d_s)
+        stream.wait_event(ev_in[b])
+        stream.wait_event(ev_out[b])  # step i-2's output has left the device buffer
+        qd, kd, vd = dev_in[b]
+        if ulysses_mode:
+            dev_out[b].copy_(ulysses.ulysses_run_step(qd, kd, vd, dims, params, sched, cache, layer=0, step=0)[0])
+        else:
+            dfs.run_step(qd, kd, vd, dims, params, sched, cache, layer=0, step=0, out=dev_out[b])
+        ev_done[b].record(stream)
+        with torch.cuda.stream(d2h_s):
+            d2h_s.wait_event(ev_done[b])
+            host_out[b].copy_(dev_out[b], non_blocking=True)
+            ev_out[b].record(d2h_s)
 
-        e2e_step()
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        n_e2e = max(3, args.steps // 2)
-        for _ in range(n_e2e):
-            e2e_step()
-        b.record(stream)
-        barrier()
-        e2e_ms = a.elapsed_time(b) / n_e2e
-        et = torch.tensor([e2e_ms], device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e2e_ms = float(et.item())
-        h2d = 3 * q.numel() * q.element_size() * world
-        d2h = out.numel() * out.element_size() * world
-        e2e = {"value": dense_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_call": e2e_ms,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+    for i in range(2):
+        e2e_step(i)
+    barrier()
+    n_e2e = max(4, args.steps)
+    a = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(n_e2e):
+        e2e_step(i)
+    d2h_s.synchronize()
+    end = torch.cuda.Event(enable_timing=True)
+    stream.wait_stream(d2h_s)
+    end.record(stream)
+    barrier()
+    e2e_ms = a.elapsed_time(end) / n_e2e
+    et = torch.tensor([e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_ms = float(et.item())
+    h2d = sum(x.numel() * x.element_size() for x in src) * world
+    d2h = src[0].numel() * src[0].element_size() * world
+    e2e = {"value": dense_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_call": e2e_ms,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "how": "public API dfs.run_step" + (" under ulysses_run_step" if ulysses_mode else "") +
+                  " on device copies of pinned host inputs, output read back every step; uploads/downloads of "
+                  "neighbouring steps overlap on copy streams"}
 
     if rank != 0:
         dist.destroy_process_group()
@@ -387,14 +452,16 @@ def main():
             cpu = cpu_baseline(wl)
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "sample": f"failed: {ex}"}
-    launches_per_step = 3 + 3 + 2 + 1  # 3 permutes, score (generic: 2 per head batch), top-K + row ptr, attention
+    # our kernels per update-step call (dfs_run_step): 3 permute(+pool), scorer prep (2 absmax, 2 fp16 split,
+    # 1 factor) + 1 tcgen05 scorer, 1 top-K, 1 LUT row pointers, 1 attention (+fused unpermute)
+    launches_per_step = 3 + 6 + 1 + 1 + 1
     res = {
         "metric": METRIC, "value": dense_flops / (ms_max * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic smooth Gaussian video fields (4 smoothing rounds), generated on device",
         "config": {"workload": wl["name"], "tokens": n, "heads": H, "heads_per_gpu": hl, "d": d, "block": B,
-                   "sub_block": Bs, "gamma": gamma, "K": K, "M": m, "parallelism": f"head-shard x{world}",
+                   "sub_block": Bs, "gamma": gamma, "K": K, "M": m, "parallelism": (f"ulysses all-to-all x{world}" if ulysses_mode else f"head-shard x{world}"),
                    "l2": "inputs 3x730 MB bf16 > 126 MB L2 (no flush needed)"},
         "ms_per_call_mask_reuse": t_reuse,
         "executed_tflop_per_call": exec_flops / 1e12, "dense_equiv_tflop_per_call": dense_flops / 1e12,
@@ -404,7 +471,7 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "roofline": {"kernel": "K5 block-sparse attention (+fused unpermute)", "bound": "tensor",
                      "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst,
-                     "peak_kind": f"{peak_kind} bf16 burst", "traffic": None,
+                     "peak_kind": f"{peak_kind} bf16 burst", "traffic": k5_traffic(args.workload, hl),
                      "algorithmic": "executed FLOPs 4*d*sum(r_u*c_v) per launch / CUDA-event duration"},
         "path_fraction_of_peak": exec_flops / (ms_max * 1e-3) / 1e12 / peak_burst,
         "e2e": e2e,
