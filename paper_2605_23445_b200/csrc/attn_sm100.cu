@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->q_empty, 1);
     for (int i = 0; i < 3; ++i) {
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->p_full[i], kSoftmaxThreads);
+      mbar_init(&bars->p_full[i], kSoftmaxThreads / 32);  // one arrive per softmax warp
       mbar_init(&bars->o_done[i], 1);
     }
     for (int i = 0; i < C::kStages; ++i) {
@@ -162,6 +162,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = ring / C::kStages;
       mbar_wait(&bars->kv_empty[slot], (use & 1) ^ 1);
       if (elect_one()) {
+#ifdef DFS_ATTN_SKIP_TMA  // experiment builds only: K/V never loaded (garbage operands)
+        mbar_arrive(&bars->kv_full[slot]);
+      }
+      if (false) {
+#endif
         mbar_expect_tx(&bars->kv_full[slot], C::kTileBytes);
         uint8_t* dst = sRing + slot * C::kTileBytes;
 #pragma unroll
@@ -238,7 +243,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
+#ifndef DFS_ATTN_SKIP_MMA  // experiment builds only (tools/attn_exp.sh): isolate the softmax side
           umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off, kHiK, C::kIdescQK, s > 0);
+#endif
         }
         umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->s_full[sb]);
@@ -257,9 +264,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t p_tmem = tmem + pb * 128;  // P_j aliases S_j (bf16 pairs)
       if (elect_one()) {
 #pragma unroll
-        for (int s = 0; s < kBN / 16; ++s)
+        for (int s = 0; s < kBN / 16; ++s) {
+#ifndef DFS_ATTN_SKIP_MMA
           umma_ts(tmem + C::kOCol, p_tmem + s * 8, v_lo + ((s * 16 * 128) >> 4), kHiK, C::kIdescPV,
                   (!first || s > 0) ? 1u : 0u);
+#endif
+        }
         umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->o_done[pb]);
       }
@@ -320,6 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars->s_full[sb], s_phase);
         if (tr) trace(p, 5 + (wg & 1) * 4, s_iter);
         tc_fence_after();
+#ifdef DFS_ATTN_SKIP_SOFTMAX  // experiment builds only: isolate the MMA/TMA side
+        (void)red_par;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+        ++s_iter;
+        continue;
+#endif
         uint32_t sv[32];
         tmem_ld32(tmem + lane_addr + sb * 128 + wg * 32, sv);
         tmem_wait_ld();
@@ -392,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         if (tr) trace(p, 7 + (wg & 1) * 4, s_iter);
-        mbar_arrive(&bars->p_full[sb]);
+        __syncwarp();  // every lane's P store has completed (tcgen05.wait::st above)
+        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
         ++s_iter;
       }
       float l;

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->acc_full[i], 1);
-      mbar_init(&bars->acc_free[i], kSoftThreads);
+      mbar_init(&bars->acc_free[i], kSoftThreads / 32);  // one arrive per softmax warp
     }
     fence_barrier_init();
   }
@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           tc_fence_before();
-          mbar_arrive(&bars->acc_free[b]);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->acc_free[b]);
           if (pass == 0) {
             float mx = l[0];
 #pragma unroll

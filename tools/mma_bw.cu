@@ -37,6 +37,44 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, unsigned long lo
   if (threadIdx.x == 0) {
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+      if (mode == 8 || mode == 9) {  // 3 S buffers: QK_{j+2} -> S[(j+2)%3], PV_j reads P_j from S[j%3]
+        const uint32_t sq = ((it + 2) % 3) * 128, sp = (it % 3) * 128;
+        if (mode == 8) {  // K5 r1 order: QK_{j+2} then PV_j (the next QK overwrites the buffer PV_j just read)
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
+            umma_f16(tmem + sq, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024), idesc, s > 0);
+          }
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            umma_f16_ts(tmem + 384, tmem + sp + s * 8, smem_desc_sw128(b + s * 16 * 128, 16384, 1024),
+                        idesc_bf16_f32(128, n_dim, false, true), 1);
+        } else {  // PV_j then QK_{j+2}
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            umma_f16_ts(tmem + 384, tmem + sp + s * 8, smem_desc_sw128(b + s * 16 * 128, 16384, 1024),
+                        idesc_bf16_f32(128, n_dim, false, true), 1);
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
+            umma_f16(tmem + sq, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024), idesc, s > 0);
+          }
+        }
+        continue;
+      }
+      if (mode == 7) {  // K5 order, unrolled: 8 SS (QK into S[it&1]) then 8 TS (PV into O), per iteration
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
+          umma_f16(tmem + (it & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024),
+                   idesc, s > 0);
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          umma_f16_ts(tmem + 256, tmem + (it & 1) * 128 + s * 8, smem_desc_sw128(b + s * 16 * 128, 16384, 1024),
+                      idesc_bf16_f32(128, n_dim, false, true), 1);
+        continue;
+      }
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
@@ -54,6 +92,14 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, unsigned long lo
           else
             umma_f16(tmem + (it & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024),
                      idesc, s > 1);
+        } else if (mode == 5) {  // TS with an MN-major B operand (K5's V: 64-col chunks, LBO = 16 KB)
+          const uint32_t vb = b + s * 16 * 128;
+          umma_f16_ts(tmem + (it & 1) * 128, tmem + 384 + s * 8, smem_desc_sw128(vb, 16384, 1024),
+                      idesc_bf16_f32(128, n_dim, false, true), s > 0);
+        } else if (mode == 6) {  // SS with an MN-major B operand
+          const uint32_t vb = b + s * 16 * 128;
+          umma_f16(tmem + (it & 1) * 128, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(vb, 16384, 1024),
+                   idesc_bf16_f32(128, n_dim, false, true), s > 0);
         } else {  // mode 4: 8 SS into S then 8 TS into O (current K5 issue order), per pair of its
           if (it & 1)
             umma_f16_ts(tmem + 256, tmem + 384 + s * 8, smem_desc_sw128(b + off, 16, 1024), idesc, s > 0);
@@ -102,7 +148,12 @@ KFn pick(int mode, int n) {
     case 1: return pick_n<1>(n);
     case 2: return pick_n<2>(n);
     case 3: return pick_n<3>(n);
-    default: return pick_n<4>(n);
+    case 4: return pick_n<4>(n);
+    case 5: return pick_n<5>(n);
+    case 6: return pick_n<6>(n);
+    case 7: return pick_n<7>(n);
+    case 8: return pick_n<8>(n);
+    default: return pick_n<9>(n);
   }
 }
 
@@ -125,10 +176,13 @@ int main() {
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
   const int smem = 65536 + 65536 + 1024;
   const int iters = 4000;
-  for (int mode = 0; mode < 5; ++mode)
+  for (int mode = 0; mode < 10; ++mode)
     for (int n : {64, 128, 256})
-      for (int tma : {0}) {
-        if (n == 256 && mode >= 2) continue;
+      for (int tma : {0, 4000, 8000}) {
+        if (n == 256 && mode >= 2 && mode < 5) continue;
+        if (n == 256 && mode >= 5) continue;
+        if (tma && !(mode >= 7 || mode == 0) ) continue;
+        if (n != 128 && tma) continue;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -143,9 +197,9 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         unsigned long long c[148];
         cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
-        const double flops = 2.0 * 128 * n * 16 * 8.0 * iters * 148;
-        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8"}[mode], n, tma,
-               double(c[0]) / (iters * 8), ms, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+        const double flops = 2.0 * 128 * n * 16 * 8.0 * iters * 148 * (mode >= 7 ? 2 : 1);
+        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8", "TS-MNmajorB", "SS-MNmajorB", "K5:SS8,TS8(P=S)", "3buf:QK(j+2),PV(j)", "3buf:PV(j),QK(j+2)"}[mode], n, tma,
+               double(c[0]) / (iters * 8 * (mode >= 7 ? 2 : 1)), ms, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
 }

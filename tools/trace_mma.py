@@ -1,24 +1,24 @@
+"""MMA-warp timeline of one CTA of K5 at HY (needs a -DDFS_ATTN_TRACE_BUILD library via DFS_B200_LIB).
+Events: 0/1 = kv_full wait start/done per ring entry, 2/3 = p_full wait start/done per PV."""
 import os, sys, numpy as np, torch
 sys.path.insert(0, '.')
 os.environ['DFS_ATTN_TRACE'] = 'gpurun_out/attn_trace.bin'
 import paper_2605_23445_b200 as m
 from paper_2605_23445_b200 import ops
-H, n, d, k = 24, 118800, 128, 93
-g = torch.Generator().manual_seed(0)
-q, kk, v = (torch.randn(H, n, d, generator=g).bfloat16().cuda() for _ in range(3))
-mq = -(-n // 128)
-lut = torch.stack([torch.stack([torch.randperm(mq, generator=g)[:k].sort().values for _ in range(mq)]) for _ in range(H)]).int().cuda()
-ptr = ops.lut_row_ptr(H, mq, k)
+from bench import smooth_fields
+dims, H, d = (33, 45, 80), 24, 128
+n = 33 * 45 * 80
+q, k, v = smooth_fields(dims, H, d, 1, torch.device('cuda'))
+perm = m.hilbert3d_order(dims)
+qh, pq = ops.permute_to_hnd(q, perm, 16); kh, pk = ops.permute_to_hnd(k, perm, 16); vh, _ = ops.permute_to_hnd(v, perm, 0)
+S = ops.score_pooled(pq, pk, n, m.ScoringParams(128, 16)); lut = m.topk_lut(S, 0.1); ptr = ops.lut_row_ptr(H, 929, 93)
 os.makedirs('gpurun_out', exist_ok=True)
-o = m.sparse_attention_csr(q, kk, v, ptr, lut.reshape(-1), 128); torch.cuda.synchronize()
+o = m.sparse_attention_csr(qh, kh, vh, ptr, lut.reshape(-1), 128); torch.cuda.synchronize()
 t = np.fromfile('gpurun_out/attn_trace.bin', dtype=np.uint64).reshape(16, 256).astype(np.int64)
-t0 = t[0, 100]
-# ring index r: even = K (QK), odd = V (PV) roughly; print a window
-print('ring r: kv_wait_start, +wait, next event delta')
-for r in range(100, 112):
-    print(r, t[0, r] - t0, t[1, r] - t[0, r], t[0, r + 1] - t[1, r])
-print('pv i: p_wait_start, p_wait')
-for i in range(50, 56):
-    print(i, t[2, i] - t0, t[3, i] - t[2, i])
-per = np.diff(t[0, 100:200:2])
-print('period per 2 ring entries (1 block):', per.mean(), 'kv wait mean', (t[1, 100:200] - t[0, 100:200]).mean(), 'p wait mean', (t[3, 50:100] - t[2, 50:100]).mean())
+r0, r1 = 100, 200  # ring entries (2 per block)
+kvw = t[1, r0:r1] - t[0, r0:r1]
+gap = t[0, r0 + 1:r1 + 1] - t[1, r0:r1]  # kv wait done -> next kv wait start (issue work + p wait)
+print("ring period", np.diff(t[0, r0:r1]).mean(), "kv wait", kvw.mean(), "done->next", gap.mean())
+p0, p1 = 50, 100
+print("PV: p wait", (t[3, p0:p1] - t[2, p0:p1]).mean(), "PV period", np.diff(t[2, p0:p1]).mean())
+print("ring entries:", [(int(t[0, i] - t[0, r0]), int(t[1, i] - t[0, i])) for i in range(r0, r0 + 12)])
