@@ -472,8 +472,12 @@ def main():
         "roofline": {"kernel": "K5 block-sparse attention (+fused unpermute)", "bound": "tensor",
                      "achieved": achieved, "peak": peak_burst, "unit": "TFLOP/s", "frac": achieved / peak_burst,
                      "peak_kind": f"{peak_kind} bf16 burst", "traffic": k5_traffic(args.workload, hl),
+                     "traffic_unit": "DRAM bytes per launch (ncu, read+write)",
+                     "algorithmic_bytes": 4.0 * n * hl * d * 2,
+                     "peak_sustained": peak_sus, "frac_sustained": achieved / peak_sus,
                      "algorithmic": "executed FLOPs 4*d*sum(r_u*c_v) per launch / CUDA-event duration"},
         "path_fraction_of_peak": exec_flops / (ms_max * 1e-3) / 1e12 / peak_burst,
+        "path_fraction_of_sustained_peak": exec_flops / (ms_max * 1e-3) / 1e12 / peak_sus,
         "e2e": e2e,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
