@@ -61,6 +61,8 @@ struct SParams {
   int64_t heads, qvalid, kvalid, m, subs, nrt, nkt, items;
   const float* fac;   // [H]: scale_log2 / (sq * sk)
   double* S;
+  float* tsum;        // per-CTA scratch [gridDim][m][128]: unnormalised row tile sums
+  float* tmax;        // per-CTA scratch [gridDim][nkt * kSWG][128]: the max each slice used
 };
 
 struct SBars {
@@ -70,6 +72,14 @@ struct SBars {
   uint32_t tmem_base;
 };
 
+// One pass over the pooled keys per 128-row stripe. Each softmax slice keeps an
+// exact online (max, sum) and writes, per key block v of its columns, the
+// unnormalised sub-row tile sum t_rv = sum_c 2^(l_rc - m_slice) together with the
+// slice max it used; after the stripe (max, sum) is merged across the slices and a
+// fix-up pass turns t_rv into probabilities, p = t_rv 2^(m_used - m_row) / z_row,
+// summed over the SUBS sub-rows of each query block. The per-CTA scratch lives in
+// L2 (it is re-read right after it is written), so the second GEMM + exp pass of a
+// two-pass softmax is replaced by one L2 round trip of 4 bytes per (row, block).
 template <int D, int SUBS>
 __global__ void __launch_bounds__(kThreads, 1)
     score_sm100_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
@@ -77,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        const SParams p) {
   using C = SCfg<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   SBars* bars = reinterpret_cast<SBars*>(smem + C::kBarOff);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -100,149 +110,176 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bars->tmem_base;
 
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t q_phase = 0, ring = 0;
-      for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
-        const int h = int(it / p.nrt), rt = int(it % p.nrt);
-        mbar_wait(&bars->q_empty, q_phase ^ 1);
-        q_phase ^= 1;
+    // ============ TMA producer (warp-uniform loop, one elected lane issues) ============
+    uint32_t q_phase = 0, ring = 0;
+    for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
+      const int h = int(it / p.nrt), rt = int(it % p.nrt);
+      mbar_wait(&bars->q_empty, q_phase ^ 1);
+      q_phase ^= 1;
+      if (elect_one()) {
         mbar_expect_tx(&bars->q_full, 2 * C::kOpBytes);
         for (int c = 0; c < C::kChunks; ++c) {
           tma_load_3d(smem + C::kQOff + c * C::kChunkBytes, &tm_qh, &bars->q_full, c * 64, rt * kRows, h);
           tma_load_3d(smem + C::kQOff + C::kOpBytes + c * C::kChunkBytes, &tm_ql, &bars->q_full, c * 64, rt * kRows, h);
         }
-        for (int pass = 0; pass < 2; ++pass)
-          for (int kt = 0; kt < p.nkt; ++kt) {
-            const uint32_t slot = ring % C::kStages;
-            mbar_wait(&bars->k_empty[slot], ((ring / C::kStages) & 1) ^ 1);
-            mbar_expect_tx(&bars->k_full[slot], 2 * C::kOpBytes);
-            uint8_t* dst = smem + C::kKOff + slot * 2 * C::kOpBytes;
-            for (int c = 0; c < C::kChunks; ++c) {
-              tma_load_3d(dst + c * C::kChunkBytes, &tm_kh, &bars->k_full[slot], c * 64, kt * kKeys, h);
-              tma_load_3d(dst + C::kOpBytes + c * C::kChunkBytes, &tm_kl, &bars->k_full[slot], c * 64, kt * kKeys, h);
-            }
-            ++ring;
+      }
+      __syncwarp();
+      for (int kt = 0; kt < p.nkt; ++kt) {
+        const uint32_t slot = ring % C::kStages;
+        mbar_wait(&bars->k_empty[slot], ((ring / C::kStages) & 1) ^ 1);
+        if (elect_one()) {
+          mbar_expect_tx(&bars->k_full[slot], 2 * C::kOpBytes);
+          uint8_t* dst = smem + C::kKOff + slot * 2 * C::kOpBytes;
+          for (int c = 0; c < C::kChunks; ++c) {
+            tma_load_3d(dst + c * C::kChunkBytes, &tm_kh, &bars->k_full[slot], c * 64, kt * kKeys, h);
+            tma_load_3d(dst + C::kOpBytes + c * C::kChunkBytes, &tm_kl, &bars->k_full[slot], c * 64, kt * kKeys, h);
           }
+        }
+        __syncwarp();
+        ++ring;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      uint32_t q_phase = 0, ring = 0, acc_iter = 0;
-      const uint32_t qh = smem_u32(smem + C::kQOff), ql = qh + C::kOpBytes;
-      for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
-        mbar_wait(&bars->q_full, q_phase);
-        q_phase ^= 1;
-        for (int pass = 0; pass < 2; ++pass)
-          for (int kt = 0; kt < p.nkt; ++kt) {
-            const uint32_t slot = ring % C::kStages;
-            mbar_wait(&bars->k_full[slot], (ring / C::kStages) & 1);
-            ++ring;
-            const uint32_t b = acc_iter & 1;
-            mbar_wait(&bars->acc_free[b], ((acc_iter >> 1) & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t kh = smem_u32(smem + C::kKOff + slot * 2 * C::kOpBytes), kl = kh + C::kOpBytes;
-            const uint32_t d1 = tmem + b * 256, d2 = d1 + 128;
+    // ============ MMA issuer: D1 = Qhi Khi^T, D2 = Qhi Klo^T + Qlo Khi^T ============
+    uint32_t q_phase = 0, ring = 0, acc_iter = 0;
+    constexpr uint32_t kHi = desc_sw128_hi(1024);
+    const uint32_t qh_lo = desc_sw128_lo(smem_u32(smem + C::kQOff), 16);
+    const uint32_t ql_lo = qh_lo + (C::kOpBytes >> 4);
+    const uint32_t k_lo0 = desc_sw128_lo(smem_u32(smem + C::kKOff), 16);
+    for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
+      mbar_wait(&bars->q_full, q_phase);
+      q_phase ^= 1;
+      for (int kt = 0; kt < p.nkt; ++kt) {
+        const uint32_t slot = ring % C::kStages;
+        mbar_wait(&bars->k_full[slot], (ring / C::kStages) & 1);
+        ++ring;
+        const uint32_t b = acc_iter & 1;
+        mbar_wait(&bars->acc_free[b], ((acc_iter >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kh_lo = k_lo0 + slot * ((2 * C::kOpBytes) >> 4), kl_lo = kh_lo + (C::kOpBytes >> 4);
+        const uint32_t d1 = tmem + b * 256, d2 = d1 + 128;
+        if (elect_one()) {
 #pragma unroll
-            for (int s = 0; s < D / 16; ++s) {
-              const uint32_t off = (s >> 2) * C::kChunkBytes + (s & 3) * 32;
-              umma_f16(d1, smem_desc_sw128(qh + off, 16, 1024), smem_desc_sw128(kh + off, 16, 1024), kIdesc, s > 0);
-              umma_f16(d2, smem_desc_sw128(qh + off, 16, 1024), smem_desc_sw128(kl + off, 16, 1024), kIdesc, s > 0);
-              umma_f16(d2, smem_desc_sw128(ql + off, 16, 1024), smem_desc_sw128(kh + off, 16, 1024), kIdesc, 1);
-            }
-            umma_commit(&bars->k_empty[slot]);
-            umma_commit(&bars->acc_full[b]);
-            if (pass == 1 && kt == p.nkt - 1) umma_commit(&bars->q_empty);
-            ++acc_iter;
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
+            umma_ss(d1, qh_lo + off, kHi, kh_lo + off, kHi, kIdesc, s > 0);
+            umma_ss(d2, qh_lo + off, kHi, kl_lo + off, kHi, kIdesc, s > 0);
+            umma_ss(d2, ql_lo + off, kHi, kh_lo + off, kHi, kIdesc, 1);
           }
+          umma_commit(&bars->k_empty[slot]);
+          umma_commit(&bars->acc_full[b]);
+          if (kt == p.nkt - 1) umma_commit(&bars->q_empty);
+        }
+        __syncwarp();
+        ++acc_iter;
       }
     }
   } else {
     // kSWG warpgroups split each 128-key tile by columns (32 apiece); a thread owns one
-    // pooled query row (TMEM lane) of its slice. Pass 0 keeps a per-slice online (max,
-    // sum), merged across the slices through shared memory once per row stripe.
+    // pooled query row (TMEM lane) of its slice.
     const int wg = (warp - 2) >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
     float* red_m = reinterpret_cast<float*>(smem + C::kRedOff);
     float* red_z = red_m + kSWG * kRows;
+    float* tsum = p.tsum + int64_t(blockIdx.x) * p.m * kRows;            // [v][row]
+    float* tmax = p.tmax + int64_t(blockIdx.x) * p.nkt * kSWG * kRows;   // [kt][slice][row]
+    constexpr int G = 32 / SUBS;                                           // key blocks per slice per tile
     uint32_t acc_iter = 0;
     for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
       const int h = int(it / p.nrt), rt = int(it % p.nrt);
       const float f = p.fac[h];
       const int64_t row = int64_t(rt) * kRows + r;     // pooled query row
-      const int64_t u = row / SUBS;
-      float m = -INFINITY, z = 0.f, inv_z = 0.f;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int kt = 0; kt < p.nkt; ++kt) {
-          const uint32_t b = acc_iter & 1;
-          mbar_wait(&bars->acc_full[b], (acc_iter >> 1) & 1);
-          tc_fence_after();
-          const int64_t cbase = int64_t(kt) * kKeys + wg * 32;
-          float l[32];
+      float m = -INFINITY, z = 0.f;
+      for (int kt = 0; kt < p.nkt; ++kt) {
+        const uint32_t b = acc_iter & 1;
+        mbar_wait(&bars->acc_full[b], (acc_iter >> 1) & 1);
+        tc_fence_after();
+        const int64_t cbase = int64_t(kt) * kKeys + wg * 32;
+        float l[32];
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t a1[16], a2[16];
-            tmem_ld16(tmem + lane_addr + b * 256 + wg * 32 + c * 16, a1);
-            tmem_ld16(tmem + lane_addr + b * 256 + 128 + wg * 32 + c * 16, a2);
-            tmem_wait_ld();
+        for (int c = 0; c < 2; ++c) {
+          uint32_t a1[16], a2[16];
+          tmem_ld16(tmem + lane_addr + b * 256 + wg * 32 + c * 16, a1);
+          tmem_ld16(tmem + lane_addr + b * 256 + 128 + wg * 32 + c * 16, a2);
+          tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float x = fmaf(__uint_as_float(a2[i]), kInvLoScale, __uint_as_float(a1[i])) * f;
-              l[c * 16 + i] = (cbase + c * 16 + i < p.kvalid) ? x : -INFINITY;
-            }
+          for (int i = 0; i < 16; ++i) {
+            const float x = fmaf(__uint_as_float(a2[i]), kInvLoScale, __uint_as_float(a1[i])) * f;
+            l[c * 16 + i] = (cbase + c * 16 + i < p.kvalid) ? x : -INFINITY;
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bars->acc_free[b]);
-          if (pass == 0) {
-            float mx = l[0];
-#pragma unroll
-            for (int i = 1; i < 32; ++i) mx = fmaxf(mx, l[i]);
-            const float mn = fmaxf(m, mx);
-            if (mn > -INFINITY) {
-              float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                s0 += ex2(l[i] - mn);
-                s1 += ex2(l[i + 1] - mn);
-              }
-              z = z * ex2(m - mn) + (s0 + s1);
-              m = mn;
-            }
-          } else {
-            // probabilities (fp32, attention.cpp:120), summed over SUBS columns, then SUBS rows
-#pragma unroll
-            for (int g = 0; g < 32 / SUBS; ++g) {
-              float t = 0.f;
-#pragma unroll
-              for (int i = 0; i < SUBS; ++i) t += ex2(l[g * SUBS + i] - m) * inv_z;
-#pragma unroll
-              for (int o = 1; o < SUBS; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-              const int64_t v = (cbase + g * SUBS) / SUBS;
-              if ((lane % SUBS) == 0 && u < p.m && v < p.m) p.S[(int64_t(h) * p.m + u) * p.m + v] = double(t);
-            }
-          }
-          ++acc_iter;
         }
-        if (pass == 0) {
-          // merge the slices' (max, sum) of this row
-          red_m[wg * kRows + r] = m;
-          red_z[wg * kRows + r] = z;
-          named_bar_sync(1, kSoftThreads);
-          float mm = -INFINITY;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->acc_free[b]);
+        ++acc_iter;
+        float mx = l[0];
 #pragma unroll
-          for (int w = 0; w < kSWG; ++w) mm = fmaxf(mm, red_m[w * kRows + r]);
-          float zz = 0.f;
+        for (int i = 1; i < 32; ++i) mx = fmaxf(mx, l[i]);
+        const float mn = fmaxf(m, mx);
+        float tg[G];
+        if (mn > -INFINITY) {
+          float s = 0.f;
 #pragma unroll
-          for (int w = 0; w < kSWG; ++w) {
-            const float mw = red_m[w * kRows + r];
-            if (mw > -INFINITY) zz += red_z[w * kRows + r] * ex2(mw - mm);
+          for (int g = 0; g < G; ++g) {
+            float t = 0.f;
+#pragma unroll
+            for (int i = 0; i < SUBS; ++i) t += ex2(l[g * SUBS + i] - mn);
+            tg[g] = t;
+            s += t;
           }
-          named_bar_sync(1, kSoftThreads);  // slots are rewritten by the next stripe
-          m = mm;
-          inv_z = 1.f / zz;
+          z = z * ex2(m - mn) + s;
+          m = mn;
+        } else {
+#pragma unroll
+          for (int g = 0; g < G; ++g) tg[g] = 0.f;
+        }
+        // coalesced across the warp: 32 consecutive rows per (v) / (kt, slice) entry
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int64_t v = (cbase + g * SUBS) / SUBS;
+          if (v < p.m) tsum[v * kRows + r] = tg[g];
+        }
+        tmax[(int64_t(kt) * kSWG + wg) * kRows + r] = m;
+      }
+      // merge the slices' (max, sum) of this row
+      red_m[wg * kRows + r] = m;
+      red_z[wg * kRows + r] = z;
+      named_bar_sync(1, kSoftThreads);  // also orders the tsum/tmax stores before the fix-up reads
+      float mm = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kSWG; ++w) mm = fmaxf(mm, red_m[w * kRows + r]);
+      float zz = 0.f;
+#pragma unroll
+      for (int w = 0; w < kSWG; ++w) {
+        const float mw = red_m[w * kRows + r];
+        if (mw > -INFINITY) zz += red_z[w * kRows + r] * ex2(mw - mm);
+      }
+      const float inv_z = 1.f / zz;
+      // fix-up: probabilities (fp32, attention.cpp:120) summed over SUBS sub-rows, fp64 S;
+      // warpgroup wg takes every kSWG-th key block
+      const int64_t u = row / SUBS;
+      constexpr int kU = 8;  // independent L2 loads in flight per thread
+      for (int64_t v0 = wg; v0 < p.m; v0 += kSWG * kU) {
+        float t[kU], mu[kU];
+#pragma unroll
+        for (int i = 0; i < kU; ++i) {
+          const int64_t v = v0 + int64_t(i) * kSWG;
+          const int64_t col = v * SUBS;
+          const int kt = int(col / kKeys), sl = int((col % kKeys) / 32);
+          t[i] = v < p.m ? tsum[v * kRows + r] : 0.f;
+          mu[i] = v < p.m ? tmax[(int64_t(kt) * kSWG + sl) * kRows + r] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < kU; ++i) {
+          const int64_t v = v0 + int64_t(i) * kSWG;
+          float pr = t[i] > 0.f ? t[i] * ex2(mu[i] - mm) * inv_z : 0.f;
+#pragma unroll
+          for (int o = 1; o < SUBS; o <<= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+          if ((lane % SUBS) == 0 && u < p.m && v < p.m) p.S[(int64_t(h) * p.m + u) * p.m + v] = double(pr);
         }
       }
+      named_bar_sync(1, kSoftThreads);  // slots and scratch are rewritten by the next stripe
     }
   }
   tc_fence_before();
@@ -314,9 +351,12 @@ bool score_sm100_supports(int64_t d, int64_t block, int64_t sub_block) {
 }
 
 int64_t score_sm100_ws_bytes(int64_t heads, int64_t n, int64_t d, int64_t block, int64_t sub_block) {
-  (void)block;
   const int64_t valid = ceil_div(n, sub_block);
-  return 4 * heads * valid * d * 2 /* qh ql kh kl */ + 2 * heads * 4 /* absmax */ + heads * 4 /* fac */ + 256;
+  const int64_t m = ceil_div(n, block);
+  const int64_t nkt = ceil_div(valid, int64_t(kKeys));
+  const int64_t scratch = int64_t(kNumSMs) * (m + nkt * kSWG) * kRows * 4;  // per-CTA tsum + tmax
+  return 4 * heads * valid * d * 2 /* qh ql kh kl */ + 2 * heads * 4 /* absmax */ + heads * 4 /* fac */ + 256 +
+         scratch + 256;
 }
 
 int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
@@ -331,6 +371,11 @@ int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t 
   __half* kl = kh + heads * per_head;
   unsigned* amax = reinterpret_cast<unsigned*>(kl + heads * per_head);
   float* fac = reinterpret_cast<float*>(amax + 2 * heads);
+  const uintptr_t sc = (reinterpret_cast<uintptr_t>(fac + heads) + 255) & ~uintptr_t(255);
+  float* tsum = reinterpret_cast<float*>(sc);
+  const int64_t m_blocks = ceil_div(n, block), nkt_keys = ceil_div(valid, int64_t(kKeys));
+  float* tmax = tsum + int64_t(kNumSMs) * m_blocks * kRows;
+  (void)nkt_keys;
   DFS_CUDA_CHECK(cudaMemsetAsync(amax, 0, sizeof(unsigned) * size_t(2 * heads), stream));
   dim3 g(unsigned(ceil_div(per_head, 256) < 64 ? ceil_div(per_head, 256) : 64), unsigned(heads));
   absmax_kernel<<<g, 256, 0, stream>>>(pq, per_head, int(heads), amax);
@@ -357,6 +402,8 @@ int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t 
   p.items = heads * p.nrt;
   p.fac = fac;
   p.S = S;
+  p.tsum = tsum;
+  p.tmax = tmax;
   const int subs = int(p.subs);
   if (d == 128) {
     switch (subs) {
