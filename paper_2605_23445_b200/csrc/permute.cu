@@ -50,7 +50,7 @@ __device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& u, float (&x)
 // One CTA = `rows` consecutive destination rows (a pooling group when pooling)
 // x all heads. Thread slots walk (head, 16B column chunk).
 template <typename T, bool kPool, bool kScatter>
-__global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ src, int src_layout,
+__global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src, int src_layout,
                                                       T* __restrict__ dst, int dst_layout,
                                                       const uint32_t* __restrict__ idx, int64_t n,
                                                       int64_t heads, int64_t d, int rows,
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256) permute_kernel(const T* __restrict__ src,
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = 0.0;
     }
-#pragma unroll 4
+#pragma unroll 8
     for (int r = 0; r < rows; ++r) {
       const int64_t i = r0 + r;
       if (i >= n) break;
@@ -140,11 +140,15 @@ int launch(const void* src, int src_layout, void* dst, int dst_layout, const uin
   const int64_t grid = ceil_div(n, rows);
   if (grid > int64_t(INT32_MAX)) return fail(DFS_E_UNSUPPORTED, "permute: too many rows");
   if (vec_ok) {
+    // one thread per (head, 16-byte column chunk) slot when that fits a CTA: every thread
+    // then walks the CTA's rows once (no second round for a remainder of slots)
+    const int64_t slots = heads * (d / Vec<T>::N);
+    const int threads = slots <= 1024 ? int(ceil_div(slots, 32) * 32) : 256;
     if (pooled)
-      permute_kernel<T, true, kScatter><<<unsigned(grid), 256, 0, stream>>>(
+      permute_kernel<T, true, kScatter><<<unsigned(grid), threads, 0, stream>>>(
           s, src_layout, o, dst_layout, idx, n, heads, d, int(rows), pooled, pool, nonfinite);
     else
-      permute_kernel<T, false, kScatter><<<unsigned(grid), 256, 0, stream>>>(
+      permute_kernel<T, false, kScatter><<<unsigned(grid), threads, 0, stream>>>(
           s, src_layout, o, dst_layout, idx, n, heads, d, int(rows), nullptr, 1, nonfinite);
   } else {
     permute_scalar_kernel<T, kScatter><<<unsigned(grid), 256, 0, stream>>>(
