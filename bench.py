@@ -154,58 +154,94 @@ def executed_flops(lut, n, block, d):
     return float(4.0 * d * (cols * sizes[None, :]).sum().item())
 
 
+class RefSampler:
+    """The reference's own CPU path (oracle/_ref: the unmodified reference sources) on a
+    bounded sample of one call: per head the full reorder + pooled keys (timed
+    separately), then `units_per_head` (head, query-block) units of pooled scoring +
+    top-K + attend_row over the unit's K blocks, parallel over all host threads with the
+    reference's parallel_for. Extrapolated to one H-head call as
+        fixed_s * ceil(H / threads) + units_s * (H * M) / units."""
+
+    def __init__(self, wl, threads=None):
+        import ctypes as C
+
+        from oracle import ref
+
+        self.C, self.ref = C, ref
+        self.dims, self.H, self.d = wl["dims"], wl["heads"], wl["d"]
+        self.B, self.Bs, self.gamma = wl["block"], wl["sub"], wl["gamma"]
+        self.n = self.dims[0] * self.dims[1] * self.dims[2]
+        self.m = -(-self.n // self.B)
+        self.threads = threads or os.cpu_count() or 1
+        self.heads_s = min(self.H, self.threads)
+        if ref is None:
+            self.ctx = None
+            return
+        lib = ref.lib
+        lib.dfsref_sample_prepare.restype = C.c_void_p
+        lib.dfsref_sample_prepare.argtypes = [C.c_int64] * 6 + [C.c_double, C.c_int, C.c_int]
+        lib.dfsref_sample_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double)]
+        lib.dfsref_sample_free.argtypes = [C.c_void_p]
+        self.lib = lib
+        self.ctx = lib.dfsref_sample_prepare(self.dims[0], self.dims[1], self.dims[2], self.d, self.B, self.Bs,
+                                             self.gamma, self.heads_s, self.threads)
+
+    def run(self, units_per_head):
+        C = self.C
+        sec, fixed = C.c_double(), C.c_double()
+        if self.lib.dfsref_sample_run(self.ctx, units_per_head, self.threads, C.byref(sec), C.byref(fixed)):
+            raise RuntimeError(self.ref._err().decode())
+        units = self.heads_s * units_per_head
+        call_s = fixed.value * math.ceil(self.H / self.threads) + sec.value * (self.H * self.m) / units
+        return call_s, sec.value, fixed.value, units
+
+    def describe(self, call_s, units_s, fixed_s, units, reps=1):
+        return (f"reference dfs:: functions (oracle/_ref, unmodified sources) on {self.threads} host threads: "
+                f"per-head reorder + key pooling {fixed_s:.2f}s for {self.heads_s} heads, then {units} of "
+                f"{self.H * self.m} (head, query-block) units (pooled scoring + top-K + attend_row over "
+                f"K={self.ref.topk_count(self.gamma, self.m)} blocks) in {units_s:.2f}s"
+                + (f" (median of {reps})" if reps > 1 else "") +
+                f"; extrapolated to one {self.H}-head call = {call_s:.0f}s")
+
+    def close(self):
+        if self.ctx:
+            self.lib.dfsref_sample_free(self.ctx)
+            self.ctx = None
+
+
 def run_reference(args, wl):
     """Reference arm: the reference's own CPU implementation (oracle/_ref, built
     from /root/reference) on a bounded sample of the same call, all host threads."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import ctypes as C
-
-    from oracle import ref
-
     dims, H, d, B, Bs, gamma = wl["dims"], wl["heads"], wl["d"], wl["block"], wl["sub"], wl["gamma"]
     n = dims[0] * dims[1] * dims[2]
-    m = -(-n // B)
     dense_flops = 4.0 * d * n * n * H
-    if ref is None:
+    rs = RefSampler(wl)
+    if rs.ctx is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdfsref.so not built (needs "
                           "/root/reference at build time)"}))
         return
-    lib = ref.lib
-    lib.dfsref_sample_prepare.restype = C.c_void_p
-    lib.dfsref_sample_prepare.argtypes = [C.c_int64] * 6 + [C.c_double, C.c_int, C.c_int]
-    lib.dfsref_sample_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]
-    lib.dfsref_sample_free.argtypes = [C.c_void_p]
-    threads = os.cpu_count() or 1
-    heads_s = min(H, threads)
-    units_per_head = max(1, (threads * args.ref_units_per_thread) // heads_s)
-    ctx = lib.dfsref_sample_prepare(dims[0], dims[1], dims[2], d, B, Bs, gamma, heads_s, threads)
-    sec = C.c_double()
-    times = []
+    units_per_head = max(1, (rs.threads * args.ref_units_per_thread) // rs.heads_s)
+    runs = []
     for i in range(args.warmup + args.steps):
-        rc = lib.dfsref_sample_run(ctx, units_per_head, threads, C.byref(sec))
-        if rc:
-            raise RuntimeError(ref._err().decode())
+        r = rs.run(units_per_head)
         if i >= args.warmup:
-            times.append(sec.value)
-    lib.dfsref_sample_free(ctx)
-    t = statistics.median(times)
-    units = heads_s * units_per_head
-    # per-head fixed part (reorder) scales with H/heads_s; per-unit part with (H*M)/units
-    call_s = t * (H * m) / units
+            runs.append(r)
+    rs.close()
+    runs.sort(key=lambda r: r[0])
+    call_s, units_s, fixed_s, units = runs[len(runs) // 2]
     value = dense_flops / call_s / 1e12
-    sample = (f"reference dfs:: functions (oracle/_ref) on {units} of {H * m} (head, query-block) units over "
-              f"{heads_s} heads, each unit = pooled scoring + top-K + attend_row over its K={ref.topk_count(gamma, m)} "
-              f"blocks; per-head full reorder included; median of {args.steps} samples of {t:.2f}s, "
-              f"extrapolated x{H * m / units:.1f} to one {H}-head call ({call_s:.0f}s)")
+    sample = rs.describe(call_s, units_s, fixed_s, units, reps=len(runs))
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": call_s * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic iid normal (content does not change CPU op count)",
            "config": {"workload": wl["name"], "tokens": n, "heads": H, "d": d, "block": B, "sub_block": Bs,
                       "gamma": gamma},
            "impl": "reference",
-           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": rs.threads, "kind": "reference",
                             "sample": sample},
            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -213,35 +249,17 @@ def run_reference(args, wl):
 
 def cpu_baseline(wl, budget_s=20.0):
     """The same sample as the reference arm, sized to ~budget_s of CPU work (rank 0, N=1)."""
-    import ctypes as C
-
-    from oracle import ref
-
-    dims, H, d, B, Bs, gamma = wl["dims"], wl["heads"], wl["d"], wl["block"], wl["sub"], wl["gamma"]
-    n = dims[0] * dims[1] * dims[2]
-    m = -(-n // B)
-    if ref is None:
+    rs = RefSampler(wl)
+    if rs.ctx is None:
         return {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
-    lib = ref.lib
-    lib.dfsref_sample_prepare.restype = C.c_void_p
-    lib.dfsref_sample_prepare.argtypes = [C.c_int64] * 6 + [C.c_double, C.c_int, C.c_int]
-    lib.dfsref_sample_run.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_double)]
-    lib.dfsref_sample_free.argtypes = [C.c_void_p]
-    threads = os.cpu_count() or 1
-    heads_s = min(H, threads)
-    upt = max(1, int(budget_s / 0.5))  # ~0.5 s of reference work per (head, block) unit at HY
-    units_per_head = max(1, (threads * upt) // heads_s // 2)
-    ctx = lib.dfsref_sample_prepare(dims[0], dims[1], dims[2], d, B, Bs, gamma, heads_s, threads)
-    sec = C.c_double()
-    lib.dfsref_sample_run(ctx, units_per_head, threads, C.byref(sec))
-    lib.dfsref_sample_free(ctx)
-    units = heads_s * units_per_head
-    call_s = sec.value * (H * m) / units
-    return {"value": 4.0 * d * n * n * H / call_s / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
-            "sample": (f"{units} of {H * m} (head, query-block) units of the reference path (oracle/_ref) in "
-                       f"{sec.value:.1f}s on {threads} threads, extrapolated to one {H}-head call = {call_s:.0f}s"),
-            "ms_per_call": call_s * 1e3}
+    # ~0.4 s of reference work per (head, query block) unit at HY on one core
+    units_per_head = max(1, int(budget_s / 0.4) * rs.threads // rs.heads_s // 2)
+    call_s, units_s, fixed_s, units = rs.run(units_per_head)
+    rs.close()
+    d, n, H = wl["d"], rs.n, wl["heads"]
+    return {"value": 4.0 * d * n * n * H / call_s / 1e12, "unit": "TFLOP/s", "cores": rs.threads,
+            "kind": "reference", "sample": rs.describe(call_s, units_s, fixed_s, units), "ms_per_call": call_s * 1e3}
 
 
 def main():

@@ -375,7 +375,7 @@ void dfsref_sample_free(void* ctx) { delete static_cast<SampleCtx*>(ctx); }
 
 // One timed sample: per head the full reorder + pooled keys, then
 // `units_per_head` query blocks through scoring + selection + attention.
-int dfsref_sample_run(void* ctx, int units_per_head, int threads, double* seconds) {
+int dfsref_sample_run(void* ctx, int units_per_head, int threads, double* seconds, double* seconds_fixed) {
   return guarded([&] {
     SampleCtx& c = *static_cast<SampleCtx*>(ctx);
     const int heads = static_cast<int>(c.qs.size());
@@ -392,6 +392,8 @@ int dfsref_sample_run(void* ctx, int units_per_head, int threads, double* second
       (void)apply_permutation(invert_permutation(p), rv);
       pks[static_cast<size_t>(hh)] = mean_pool(c.ks[static_cast<size_t>(hh)], bs);
     });
+    const auto tf = std::chrono::steady_clock::now();
+    if (seconds_fixed) *seconds_fixed = std::chrono::duration<double>(tf - t0).count();
     parallel_for(static_cast<int64_t>(heads) * units_per_head, threads, [&](int64_t item) {
       const int hh = static_cast<int>(item / units_per_head);
       const int64_t slot = item % units_per_head;
@@ -428,7 +430,7 @@ int dfsref_sample_run(void* ctx, int units_per_head, int threads, double* second
       (void)full_attention_output(xq, ksel, vsel);
     });
     const auto t1 = std::chrono::steady_clock::now();
-    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    *seconds = std::chrono::duration<double>(t1 - tf).count();  // the sampled units only
   });
 }
 
