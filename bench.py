@@ -262,6 +262,79 @@ def cpu_baseline(wl, budget_s=20.0):
             "kind": "reference", "sample": rs.describe(call_s, units_s, fixed_s, units), "ms_per_call": call_s * 1e3}
 
 
+TRAJ_BUDGETS = {"W4": (0.15,), "W7": (0.3, 0.2, 0.1), "HY": (0.3, 0.2, 0.1), "C": (0.2,)}
+
+
+def run_trajectory_bench(args, wl, dfs, dev, world, rank, local, dist):
+    """Config W4 / W7 of BASELINE.json: masks cached across a 50-step schedule
+    (scheduler.hpp:22-28 defaults: warmup 25%, phase 25% per budget, Delta = 12)."""
+    import torch
+
+    dims, H, d, B, Bs = wl["dims"], wl["heads"], wl["d"], wl["block"], wl["sub"]
+    n = dims[0] * dims[1] * dims[2]
+    h0, h1 = rank * H // world, (rank + 1) * H // world
+    q, k, v = smooth_fields(dims, h1 - h0, d, seed=1000 + rank, device=dev)
+    budgets = TRAJ_BUDGETS.get(args.workload, (wl["gamma"],))
+    T = 50
+    sched = dfs.SparsitySchedule(total_steps=T, warmup_fraction=0.25, phase_budgets=budgets,
+                                 phase_fraction=min(0.25, 0.75 / len(budgets)), update_interval=12)
+    cache = dfs.MaskCache()
+    params = dfs.ScoringParams(B, Bs)
+    out = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    kinds = {"dense": [], "update": [], "reuse": []}
+    dense_flops_total = 0.0
+    for i in range(args.warmup):
+        dfs.run_step(q, k, v, dims, params, sched, cache, layer=0, step=i % T, out=out)
+    barrier()
+    steps = max(args.steps, T)
+    with ClockSampler(local) as clocks:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(steps):
+            s = i % T
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _, st = dfs.run_step(q, k, v, dims, params, sched, cache, layer=0, step=s, out=out)
+            b.record(stream)
+            kind = "dense" if st.dense else ("update" if any(st.mask_updated) else "reuse")
+            kinds[kind].append((a, b))
+            dense_flops_total += 4.0 * d * n * n * H
+        t1 = torch.cuda.Event(enable_timing=True)
+        t1.record(stream)
+        barrier()
+    ms = t0.elapsed_time(t1) / steps
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    per_kind = {kk: (statistics.mean(a.elapsed_time(b) for a, b in vv) if vv else None, len(vv))
+                for kk, vv in kinds.items()}
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    res = {"metric": METRIC + " (averaged over a 50-step mask-caching trajectory)",
+           "value": dense_flops_total / steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "bf16", "data": "synthetic smooth Gaussian video fields",
+           "config": {"workload": wl["name"], "schedule": {"total_steps": T, "warmup_fraction": 0.25,
+                                                          "phase_budgets": list(budgets), "update_interval": 12},
+                      "parallelism": f"head-shard x{world}"},
+           "per_step_kind_ms": {kk: {"mean_ms": m_, "count": c_} for kk, (m_, c_) in per_kind.items()},
+           "gpu_launches": None, "clocks": clocks.summary()}
+    print(json.dumps(res))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -272,6 +345,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-units-per-thread", type=int, default=20)
     ap.add_argument("--profile", action="store_true", help="only run warmup+steps of the step (for ncu)")
+    ap.add_argument("--trajectory", action="store_true",
+                    help="diffusion trajectory: T=50 steps, 25%% dense warmup, phase budgets, mask update every "
+                         "Delta=12 sparse steps (the device mask cache serves the other steps); reports per-step "
+                         "averages over the whole schedule instead of the update-step call")
     ap.add_argument("--ulysses", action="store_true",
                     help="sequence-sharded inputs [N/P, H, d]: NCCL all-to-all to heads, step, all-to-all back "
                          "(inside the timed region); default: head-sharded inputs, no collective")
@@ -300,6 +377,8 @@ def main():
     m = -(-n // B)
     h0, h1 = rank * H // world, (rank + 1) * H // world
     hl = h1 - h0
+    if args.trajectory:
+        return run_trajectory_bench(args, wl, dfs, dev, world, rank, local, dist)
     ulysses_mode = args.ulysses and world > 1
     if ulysses_mode:
         from paper_2605_23445_b200 import ulysses
