@@ -37,6 +37,29 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, unsigned long lo
   if (threadIdx.x == 0) {
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+      if (mode == 10 || mode == 11) {  // mode 8's order with K/V operands rotating through 5 ring slots of 32 KB
+        const uint32_t sq = ((it + 2) % 3) * 128, sp = (it % 3) * 128;
+        const uint32_t ring = a + 32768;  // Q at a (32 KB), ring after it
+        const uint32_t kslot = ring + uint32_t((2 * it) % 5) * 32768, vslot = ring + uint32_t((2 * it + 1) % 5) * 32768;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
+          umma_f16(tmem + sq, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(kslot + off, 16, 1024), idesc, s > 0);
+        }
+        if (mode == 11) {  // K5 commits two mbarriers after every group (kv_empty + s_full / o_done)
+          umma_commit(&tbar[0]);
+          umma_commit(&tbar[1]);
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          umma_f16_ts(tmem + 384, tmem + sp + s * 8, smem_desc_sw128(vslot + s * 16 * 128, 16384, 1024),
+                      idesc_bf16_f32(128, n_dim, false, true), 1);
+        if (mode == 11) {
+          umma_commit(&tbar[0]);
+          umma_commit(&tbar[1]);
+        }
+        continue;
+      }
       if (mode == 8 || mode == 9) {  // 3 S buffers: QK_{j+2} -> S[(j+2)%3], PV_j reads P_j from S[j%3]
         const uint32_t sq = ((it + 2) % 3) * 128, sp = (it % 3) * 128;
         if (mode == 8) {  // K5 r1 order: QK_{j+2} then PV_j (the next QK overwrites the buffer PV_j just read)
@@ -153,7 +176,9 @@ KFn pick(int mode, int n) {
     case 6: return pick_n<6>(n);
     case 7: return pick_n<7>(n);
     case 8: return pick_n<8>(n);
-    default: return pick_n<9>(n);
+    case 9: return pick_n<9>(n);
+    case 10: return pick_n<10>(n);
+    default: return pick_n<11>(n);
   }
 }
 
@@ -174,9 +199,9 @@ int main() {
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   unsigned long long* d;
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
-  const int smem = 65536 + 65536 + 1024;
+  const int smem = 32768 * 6 + 1024;
   const int iters = 4000;
-  for (int mode = 0; mode < 10; ++mode)
+  for (int mode = 0; mode < 12; ++mode)
     for (int n : {64, 128, 256})
       for (int tma : {0, 4000, 8000}) {
         if (n == 256 && mode >= 2 && mode < 5) continue;
@@ -198,7 +223,7 @@ int main() {
         unsigned long long c[148];
         cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
         const double flops = 2.0 * 128 * n * 16 * 8.0 * iters * 148 * (mode >= 7 ? 2 : 1);
-        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8", "TS-MNmajorB", "SS-MNmajorB", "K5:SS8,TS8(P=S)", "3buf:QK(j+2),PV(j)", "3buf:PV(j),QK(j+2)"}[mode], n, tma,
+        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8", "TS-MNmajorB", "SS-MNmajorB", "K5:SS8,TS8(P=S)", "3buf:QK(j+2),PV(j)", "3buf:PV(j),QK(j+2)", "3buf+5 ring slots", "3buf+ring+commits"}[mode], n, tma,
                double(c[0]) / (iters * 8 * (mode >= 7 ? 2 : 1)), ms, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;

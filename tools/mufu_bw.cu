@@ -1,11 +1,23 @@
 // Microbenchmark: MUFU.EX2 and FFMA2 throughput per SM per clock on this GPU.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mufu_bw tools/mufu_bw.cu && tools/mufu_bw
+#include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t ex2_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t ex2_f16x2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
   return y;
 }
 
@@ -20,6 +32,8 @@ __global__ void k(float* out, int iters, long long* clk) {
     for (int i = 0; i < 8; ++i) {
       if (MODE == 0) a[i] = ex2(a[i]) * -0.5f;          // MUFU + FMUL
       if (MODE == 1) a[i] = fmaf(a[i], 0.999f, 1e-3f);  // FFMA
+      if (MODE == 2) a[i] = __uint_as_float(ex2_bf16x2(__float_as_uint(a[i])) ^ 0x80008000u);  // 2 results
+      if (MODE == 3) a[i] = __uint_as_float(ex2_f16x2(__float_as_uint(a[i])) ^ 0x80008000u);
     }
   }
   long long t1 = clock64();
@@ -36,7 +50,7 @@ int main() {
   cudaMalloc(&out, 148 * 1024 * 4);
   cudaMallocManaged(&clk, 8);
   const int iters = 4096;
-  for (int mode = 0; mode < 2; ++mode)
+  for (int mode = 0; mode < 4; ++mode)
     for (int threads : {128, 256, 512, 1024}) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
@@ -44,14 +58,17 @@ int main() {
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
         if (mode == 0) k<0><<<148, threads>>>(out, iters, clk);
-        else k<1><<<148, threads>>>(out, iters, clk);
+        else if (mode == 1) k<1><<<148, threads>>>(out, iters, clk);
+        else if (mode == 2) k<2><<<148, threads>>>(out, iters, clk);
+        else k<3><<<148, threads>>>(out, iters, clk);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
       }
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
-      double ops_per_sm = double(threads) * iters * 8;
-      printf("%s threads=%4d  %.3f ms  clk=%lld  ops/clk/SM=%.2f\n", mode == 0 ? "ex2 " : "ffma", threads, ms, *clk,
+      double ops_per_sm = double(threads) * iters * 8 * (mode >= 2 ? 2 : 1);
+      const char* names[] = {"ex2.f32   ", "ffma      ", "ex2.bf16x2", "ex2.f16x2 "};
+      printf("%s threads=%4d  %.3f ms  clk=%lld  results/clk/SM=%.2f\n", names[mode], threads, ms, *clk,
              ops_per_sm / double(*clk));
     }
   return 0;
