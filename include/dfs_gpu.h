@@ -78,7 +78,8 @@ int dfs_validate_permutation(dfs_handle* h, const uint32_t* fwd, int64_t n, int*
 
 /* ================ K2/K6: permute / unpermute (curve.hpp:50,53) ============== */
 /* dst row i <- src row idx[i] for every head (curve.cpp:166 apply_permutation),
- * converting layout src_layout -> dst_layout. With pooled != NULL also emits
+ * converting layout src_layout -> dst_layout. dst may be NULL (read-only pass)
+ * when pooled and/or nonfinite is given. With pooled != NULL also emits
  * the sub-block means of the DESTINATION rows (mask_builder.cpp:12 mean_pool,
  * zero-padded last group divided by pool) as fp32 [H, ceil(n/pool), d].
  * With nonfinite != NULL atomically ORs 1 into *nonfinite when any element is
@@ -146,6 +147,11 @@ typedef struct {
   float scale;
   int force_generic; /* 1: use the SIMT kernel even when the tcgen05 one applies */
   int64_t dv;        /* head dim of v / o; 0 = d (dv != d: fp32 kernel only) */
+  /* Fused query reorder: when non-NULL, q is the [nq, H, d] raster-order (NHD)
+   * tensor and logical query row i is its row in_rows[i], gathered by TMA inside
+   * the kernel (curve.cpp:166 apply_permutation without a permuted copy of Q);
+   * k and v keep `in_layout`. */
+  const uint32_t* in_rows;
 } dfs_attn_args;
 int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream);
 

@@ -39,7 +39,7 @@ class AttnArgs(C.Structure):
     _fields_ = [("q", _p), ("k", _p), ("v", _p), ("o", _p), ("dtype", _i32), ("in_layout", _i32),
                 ("out_layout", _i32), ("heads", _i64), ("nq", _i64), ("nk", _i64), ("d", _i64),
                 ("block", _i64), ("blk_ptr", _p), ("blk_idx", _p), ("out_rows", _p), ("scale", _f),
-                ("force_generic", _i32), ("dv", _i64)]
+                ("force_generic", _i32), ("dv", _i64), ("in_rows", _p)]
 
 
 class Schedule(C.Structure):

@@ -41,7 +41,10 @@ __global__ void __launch_bounds__(128) attn_generic_kernel(dfs_attn_args a, int6
     float qr[DMAX], acc[DMAX];
 #pragma unroll
     for (int c = 0; c < DMAX; ++c) {
-      qr[c] = (active && c < d) ? to_f32<T>(q[row_offset(a.in_layout, a.nq, a.heads, d, h, i) + c]) * scale : 0.f;
+      qr[c] = (active && c < d)
+                  ? to_f32<T>(q[(a.in_rows ? row_offset(DFS_NHD, a.nq, a.heads, d, h, int64_t(a.in_rows[i]))
+                                            : row_offset(a.in_layout, a.nq, a.heads, d, h, i)) + c]) * scale
+                  : 0.f;
       acc[c] = 0.f;
     }
     float mrun = -INFINITY, l = 0.f;
@@ -136,7 +139,8 @@ __global__ void __launch_bounds__(128) attn_f64_kernel(dfs_attn_args a, int64_t 
   const int32_t beg = a.blk_ptr ? a.blk_ptr[h * mq + u] : 0;
   const int32_t end = a.blk_ptr ? a.blk_ptr[h * mq + u + 1] : int32_t(mk);
   double qv[DPL];
-  const float* qrow = q + row_offset(a.in_layout, a.nq, a.heads, d, h, row);
+  const float* qrow = q + (a.in_rows ? row_offset(DFS_NHD, a.nq, a.heads, d, h, int64_t(a.in_rows[row]))
+                                     : row_offset(a.in_layout, a.nq, a.heads, d, h, row));
 #pragma unroll
   for (int t = 0; t < DPL; ++t) {
     const int64_t c = lane + 32 * t;

@@ -74,6 +74,7 @@ struct Params {
   int out_layout;
   int in_nhd;  // 1: inputs are [N, H, d] (tensor-map coordinates (col, head, row))
   float scale_log2;
+  const uint32_t* in_rows;  // fused Q reorder: logical query row i = raster token in_rows[i] (NULL: tiles)
   unsigned long long* trace;  // debug timeline (DFS_ATTN_TRACE), NULL in production
   int64_t tiles;
 };
@@ -157,24 +158,53 @@ __global__ void __launch_bounds__(kThreads, 1)
     // warp (one coalesced load) and broadcast with shuffles, keeping the LUT's
     // global-load latency off the per-block issue path.
     uint32_t q_phase = 0, ring = 0;
-    auto load_tile = [&](const CUtensorMap* map, int64_t h, int64_t row0) {
-      const uint32_t slot = ring % C::kStages;
-      const uint32_t use = ring / C::kStages;
-      mbar_wait(&bars->kv_empty[slot], (use & 1) ^ 1);
-      if (elect_one()) {
-#ifdef DFS_ATTN_SKIP_TMA  // experiment builds only: K/V never loaded (garbage operands)
-        mbar_arrive(&bars->kv_full[slot]);
+    // Fused Q reorder (p.in_rows != NULL): Q's map is 2D over the raster [N*H, d]
+    // activations and a 128-row tile is 32 tile::gather4 loads per 64-column chunk, one
+    // per lane; lane l fetches logical rows 4l..4l+3 = raster tokens in_rows[row0+4l..].
+    // Rows past n (partial last block) repeat a valid token (padded queries are never
+    // stored). K/V are not gathered: each K/V tile is re-read by ~K query blocks, and
+    // gather4 moves only ~7 B/clk/SM (measured), so their reorder stays a one-time copy.
+    // The raster row indices are loaded before waiting for the ring slot, so their
+    // latency overlaps the wait.
+    auto gather_rows = [&](int64_t h, int64_t row0, int (&rr)[4]) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int64_t i = row0 + 4 * lane + k;
+        i = i < p.nq ? i : p.nq - 1;
+        rr[k] = int(int64_t(__ldg(p.in_rows + i)) * p.heads + h);
       }
-      if (false) {
-#endif
-        mbar_expect_tx(&bars->kv_full[slot], C::kTileBytes);
-        uint8_t* dst = sRing + slot * C::kTileBytes;
+    };
+    auto issue_tile = [&](const CUtensorMap* map, int64_t h, int64_t row0, uint8_t* dst, uint64_t* bar,
+                          const int (&rr)[4], bool gather) {
+      if (gather) {
+        if (elect_one()) mbar_expect_tx(bar, C::kTileBytes);
+        __syncwarp();
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(dst + c * C::kChunkBytes, map, &bars->kv_full[slot], c * 64, p.in_nhd ? int(h) : int(row0),
+          tma_gather4(dst + c * C::kChunkBytes + lane * 512, map, bar, c * 64, rr[0], rr[1], rr[2], rr[3]);
+        __syncwarp();
+        return;
+      }
+      if (elect_one()) {
+        mbar_expect_tx(bar, C::kTileBytes);
+#pragma unroll
+        for (int c = 0; c < C::kChunks; ++c)
+          tma_load_3d(dst + c * C::kChunkBytes, map, bar, c * 64, p.in_nhd ? int(h) : int(row0),
                       p.in_nhd ? int(row0) : int(h));
       }
       __syncwarp();
+    };
+    auto load_tile = [&](const CUtensorMap* map, int64_t h, int64_t row0) {
+      const uint32_t slot = ring % C::kStages;
+      const uint32_t use = ring / C::kStages;
+      const int rr[4] = {0, 0, 0, 0};
+      mbar_wait(&bars->kv_empty[slot], (use & 1) ^ 1);
+#ifdef DFS_ATTN_SKIP_TMA  // experiment builds only: K/V never loaded (garbage operands)
+      if (elect_one()) mbar_arrive(&bars->kv_full[slot]);
+      __syncwarp();
+#else
+      issue_tile(map, h, row0, sRing + slot * C::kTileBytes, &bars->kv_full[slot], rr, false);
+#endif
       ++ring;
     };
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
@@ -183,14 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_list(p, tile, h, u, beg, cnt);
       mbar_wait(&bars->q_empty, q_phase ^ 1);
       q_phase ^= 1;
-      if (elect_one()) {
-        mbar_expect_tx(&bars->q_full, C::kTileBytes);
-#pragma unroll
-        for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(sQ + c * C::kChunkBytes, &tm_q, &bars->q_full, c * 64, p.in_nhd ? int(h) : int(u * kBM),
-                      p.in_nhd ? int(u * kBM) : int(h));
+      {
+        int rr[4] = {0, 0, 0, 0};
+        if (p.in_rows) gather_rows(h, u * kBM, rr);
+        issue_tile(&tm_q, h, u * kBM, sQ, &bars->q_full, rr, p.in_rows != nullptr);
       }
-      __syncwarp();
       // key-block list window: entries [win, win + 32) held one per lane
       int32_t win = -64, lut_reg = 0;
       auto blk = [&](int32_t j) -> int32_t {
@@ -511,6 +538,21 @@ int make_map(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t 
   return DFS_OK;
 }
 
+// 2D map over rows x d bf16 for tile::gather4: box {64 columns, 1 row}, SWIZZLE_128B
+int make_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_t d) {
+  EncodeFn enc = get_encode();
+  if (!enc) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (rows >= (int64_t(1) << 31)) return fail(DFS_E_UNSUPPORTED, "attn_sm100: N*H too large for row gather");
+  cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(d) * 2};
+  cuuint32_t box[2] = {64, 1}, estr[2] = {1, 1};
+  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled (gather) failed");
+  return DFS_OK;
+}
+
 template <int D, int POLY>
 int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const Params& p,
                   cudaStream_t stream) {
@@ -538,7 +580,11 @@ template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   CUtensorMap mq, mk, mv;
   int rc;
-  if ((rc = make_map(&mq, a.q, a.in_layout, a.nq, a.heads, D))) return rc;
+  if (a.in_rows) {  // Q: 2D row-gather map over the raster [N*H, d] activations
+    if ((rc = make_gather_map(&mq, a.q, a.nq * a.heads, D))) return rc;
+  } else if ((rc = make_map(&mq, a.q, a.in_layout, a.nq, a.heads, D))) {
+    return rc;
+  }
   if ((rc = make_map(&mk, a.k, a.in_layout, a.nk, a.heads, D))) return rc;
   if ((rc = make_map(&mv, a.v, a.in_layout, a.nk, a.heads, D))) return rc;
   Params p;
@@ -554,6 +600,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   p.out_layout = a.out_layout;
   p.in_nhd = a.in_layout == DFS_NHD;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.in_rows = a.in_rows;
   p.tiles = p.mq * a.heads;
   p.trace = nullptr;
 #ifdef DFS_ATTN_TRACE_BUILD
@@ -602,6 +649,7 @@ int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads
 bool attn_sm100_supports(const dfs_attn_args& a) {
   if (a.dtype != DFS_BF16 || a.block != 128 || (a.d != 64 && a.d != 128)) return false;
   if (a.dv > 0 && a.dv != a.d) return false;
+  if (a.in_rows && a.nq >= (int64_t(1) << 31) / a.heads) return false;
   const void* ptrs[4] = {a.q, a.k, a.v, a.o};
   for (const void* ptr : ptrs)
     if (reinterpret_cast<uintptr_t>(ptr) & 15) return false;

@@ -136,11 +136,11 @@ struct dfs_handle {
   std::map<int, LayerMasks> masks;  // keyed by layer
   // workspaces
   Buf scratch_i32, flag;
-  Buf q_hnd, k_hnd, v_hnd, pooled_q, pooled_k, scores, score_ws, lut, sel, counts;
+  Buf k_hnd, v_hnd, pooled_q, pooled_k, scores, score_ws, lut, sel, counts;
   Buf tmp_ptr, tmp_idx;
   int64_t total_bytes() const {
     int64_t t = 0;
-    for (const Buf* b : {&scratch_i32, &flag, &q_hnd, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
+    for (const Buf* b : {&scratch_i32, &flag, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
                          &lut, &sel, &counts, &tmp_ptr, &tmp_idx})
       t += int64_t(b->bytes);
     return t;
@@ -321,7 +321,7 @@ int dfs_validate_permutation(dfs_handle* h, const uint32_t* fwd, int64_t n, int*
 int dfs_permute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype, const uint32_t* idx,
                      int64_t n, int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite,
                      dfs_stream stream) {
-  if (!src || !dst || !idx) return fail(DFS_E_INVALID, "permute_rows: null pointer");
+  if (!src || !idx || (!dst && !pooled && !nonfinite)) return fail(DFS_E_INVALID, "permute_rows: null pointer");
   return permute_rows_impl(src, src_layout, dst, dst_layout, dtype, idx, n, heads, d, pooled, pool, nonfinite,
                            false, as_stream(stream));
 }
@@ -698,9 +698,12 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   const bool update_any = !need.empty();
 
   int rc;
+  // Reorder: Q is gathered by K5 itself (TMA tile::gather4 by `fwd`, once per query
+  // tile), so an update step only reads q for its pooled sub-block rows; K and V are
+  // re-read by every query block that selects them, so they get one permuted [H, N, d]
+  // copy each (K with the pooled rows fused in).
   const size_t tok_bytes = sizeof(__nv_bfloat16) * size_t(n * H * d);
-  if ((rc = h->q_hnd.ensure(tok_bytes)) || (rc = h->k_hnd.ensure(tok_bytes)) || (rc = h->v_hnd.ensure(tok_bytes)))
-    return rc;
+  if ((rc = h->k_hnd.ensure(tok_bytes)) || (rc = h->v_hnd.ensure(tok_bytes))) return rc;
   const int64_t pv = ceil_div(n, Bs);
   float* pq = nullptr;
   float* pk = nullptr;
@@ -710,11 +713,14 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       return rc;
     pq = h->pooled_q.as<float>();
     pk = h->pooled_k.as<float>();
+    if ((rc = permute_rows_impl(a->q, DFS_NHD, nullptr, DFS_HND, DFS_BF16, fwd, n, H, d, pq, Bs, a->nonfinite, false,
+                                s)))
+      return rc;
+  } else if (a->nonfinite && (rc = finite_check_impl(a->q, n * H * d, DFS_BF16, a->nonfinite, s))) {
+    return rc;
   }
-  if ((rc = permute_rows_impl(a->q, DFS_NHD, h->q_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pq, Bs, a->nonfinite,
-                              false, s)) ||
-      (rc = permute_rows_impl(a->k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, Bs, a->nonfinite,
-                              false, s)) ||
+  if ((rc = permute_rows_impl(a->k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, Bs, a->nonfinite, false,
+                              s)) ||
       (rc = permute_rows_impl(a->v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, a->nonfinite,
                               false, s)))
     return rc;
@@ -778,12 +784,13 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   }
 
   dfs_attn_args at{};
-  at.q = h->q_hnd.p;
+  at.q = a->q;  // raster [N, H, d]: K5 gathers the Hilbert-ordered query rows itself
   at.k = h->k_hnd.p;
   at.v = h->v_hnd.p;
   at.o = a->o;
   at.dtype = DFS_BF16;
   at.in_layout = DFS_HND;
+  at.in_rows = fwd;
   at.out_layout = DFS_NHD;
   at.heads = H;
   at.nq = n;

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
       const int64_t di = kScatter ? int64_t(idx[i]) : i;
       if (si >= n || di >= n) continue;  // invalid permutation entry: no wild access
       const uint4 u = *reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c);
-      *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) = u;
+      if (dst) *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) = u;
       if (kPool || nonfinite) {
         float x[V];
         unpack<T>(u, x);
@@ -119,7 +119,7 @@ __global__ void permute_scalar_kernel(const T* __restrict__ src, int src_layout,
       const int64_t di = kScatter ? int64_t(idx[i]) : i;
       if (si >= n || di >= n) continue;
       const T x = src[row_offset(src_layout, n, heads, d, h, si) + c];
-      dst[row_offset(dst_layout, n, heads, d, h, di) + c] = x;
+      if (dst) dst[row_offset(dst_layout, n, heads, d, h, di) + c] = x;
       const float xf = to_f32<T>(x);
       acc += double(xf);
       bad |= !isfinite(xf);
@@ -134,6 +134,7 @@ int launch(const void* src, int src_layout, void* dst, int dst_layout, const uin
            int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite, cudaStream_t stream) {
   const T* s = static_cast<const T*>(src);
   T* o = static_cast<T*>(dst);
+  // dst == NULL: read-only pass (pooled rows and/or the finite check of a gathered order)
   const bool vec_ok = d % Vec<T>::N == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
                       (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (!pooled || pool <= 64);
   const int64_t rows = pooled ? pool : 16;

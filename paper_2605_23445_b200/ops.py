@@ -395,12 +395,13 @@ def build_mask(q: torch.Tensor, k: torch.Tensor, params: ScoringParams, budget: 
 
 
 def _attn_call(q, k, v, out, heads, nq, nk, d, block, blk_ptr, blk_idx, in_layout, out_layout,
-               out_rows=None, force_generic=False, scale=0.0):
+               out_rows=None, force_generic=False, scale=0.0, in_rows=None):
     a = capi.AttnArgs(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), _dtype_code(q), in_layout,
                       out_layout, heads, nq, nk, d, block,
                       0 if blk_ptr is None else blk_ptr.data_ptr(),
                       0 if blk_idx is None else blk_idx.data_ptr(),
-                      0 if out_rows is None else out_rows.data_ptr(), float(scale), int(force_generic))
+                      0 if out_rows is None else out_rows.data_ptr(), float(scale), int(force_generic), 0,
+                      0 if in_rows is None else in_rows.data_ptr())
     capi.call("dfs_sparse_attn_fwd", default_handle().ptr, C.byref(a), _stream())
 
 
@@ -470,9 +471,14 @@ def full_attention_output(q, k, v, block: int = 128, force_generic: bool = False
 
 
 def sparse_attention_csr(q, k, v, blk_ptr, blk_idx, block, layout=capi.DFS_HND, out_layout=None,
-                         out_rows=None, out=None, force_generic=False):
-    """Batched K5 over all heads: q/k/v [H, N, d] (HND) or [N, H, d] (NHD) bf16."""
-    if layout == capi.DFS_HND:
+                         out_rows=None, out=None, force_generic=False, in_rows=None):
+    """Batched K5 over all heads: q/k/v [H, N, d] (HND) or [N, H, d] (NHD) bf16.
+
+    in_rows (NHD only): logical row i is raster row in_rows[i] (the reorder fused into K5)."""
+    if in_rows is not None:  # q is the raster [N, H, d] tensor, gathered inside K5
+        nq, h, d = q.shape
+        nk = k.shape[1] if layout == capi.DFS_HND else k.shape[0]
+    elif layout == capi.DFS_HND:
         h, nq, d = q.shape
         nk = k.shape[1]
     else:
@@ -483,8 +489,17 @@ def sparse_attention_csr(q, k, v, blk_ptr, blk_idx, block, layout=capi.DFS_HND, 
         out = torch.empty((h, nq, d) if out_layout == capi.DFS_HND else (nq, h, d), dtype=q.dtype,
                           device=q.device)
     _attn_call(q, k, v, out, h, nq, nk, d, block, blk_ptr, blk_idx, layout, out_layout, out_rows,
-               force_generic)
+               force_generic, in_rows=in_rows)
     return out
+
+
+def pool_gathered(x: torch.Tensor, perm: Permutation, pool: int, nonfinite: torch.Tensor | None = None):
+    """K2 read-only: sub-block means of x [N, H, d] taken in `perm` order -> fp32 [H, ceil(N/pool), d]."""
+    n, h, d = x.shape
+    pooled = torch.empty((h, (n + pool - 1) // pool, d), dtype=torch.float32, device=x.device)
+    capi.call("dfs_permute_rows", _ptr(x), capi.DFS_NHD, None, capi.DFS_HND, _dtype_code(x), _ptr(perm.forward),
+              n, h, d, _ptr(pooled), pool, _ptr(nonfinite), _stream())
+    return pooled
 
 
 # --------------------------------------------------------------------------- #
