@@ -196,37 +196,62 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars->acc_full[b], (acc_iter >> 1) & 1);
         tc_fence_after();
         const int64_t cbase = int64_t(kt) * kKeys + wg * 32;
-        float l[32];
+        // logits l = (D1 + D2 / 2^11) * f in packed fp32x2 arithmetic; only the tile holding
+        // the end of the valid pooled keys masks (warp-uniform branch)
+        uint64_t l2[16];
+        {
+          const uint64_t f2 = f2_pack(f, f), g2 = f2_pack(f * kInvLoScale, f * kInvLoScale);
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t a1[16], a2[16];
-          tmem_ld16(tmem + lane_addr + b * 256 + wg * 32 + c * 16, a1);
-          tmem_ld16(tmem + lane_addr + b * 256 + 128 + wg * 32 + c * 16, a2);
-          tmem_wait_ld();
+          for (int c = 0; c < 2; ++c) {
+            uint32_t a1[16], a2[16];
+            tmem_ld16(tmem + lane_addr + b * 256 + wg * 32 + c * 16, a1);
+            tmem_ld16(tmem + lane_addr + b * 256 + 128 + wg * 32 + c * 16, a2);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float x = fmaf(__uint_as_float(a2[i]), kInvLoScale, __uint_as_float(a1[i])) * f;
-            l[c * 16 + i] = (cbase + c * 16 + i < p.kvalid) ? x : -INFINITY;
+            for (int i = 0; i < 8; ++i)
+              l2[c * 8 + i] = f2_fma(f2_pack(__uint_as_float(a2[2 * i]), __uint_as_float(a2[2 * i + 1])), g2,
+                                     f2_mul(f2_pack(__uint_as_float(a1[2 * i]), __uint_as_float(a1[2 * i + 1])), f2));
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->acc_free[b]);
         ++acc_iter;
-        float mx = l[0];
+        if (cbase + 32 > p.kvalid) {
 #pragma unroll
-        for (int i = 1; i < 32; ++i) mx = fmaxf(mx, l[i]);
+          for (int i = 0; i < 16; ++i) {
+            float x0, x1;
+            f2_unpack(l2[i], x0, x1);
+            if (cbase + 2 * i >= p.kvalid) x0 = -INFINITY;
+            if (cbase + 2 * i + 1 >= p.kvalid) x1 = -INFINITY;
+            l2[i] = f2_pack(x0, x1);
+          }
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float x0, x1;
+          f2_unpack(l2[i], x0, x1);
+          mx = fmaxf(mx, fmaxf(x0, x1));
+        }
         const float mn = fmaxf(m, mx);
         float tg[G];
         if (mn > -INFINITY) {
+          const uint64_t nm2 = f2_pack(-mn, -mn);
           float s = 0.f;
 #pragma unroll
           for (int g = 0; g < G; ++g) {
-            float t = 0.f;
+            uint64_t t2 = 0;  // two independent fp32 chains per group
 #pragma unroll
-            for (int i = 0; i < SUBS; ++i) t += ex2(l[g * SUBS + i] - mn);
-            tg[g] = t;
-            s += t;
+            for (int i = 0; i < SUBS / 2; ++i) {
+              float x0, x1;
+              f2_unpack(f2_add(l2[g * (SUBS / 2) + i], nm2), x0, x1);
+              t2 = f2_add(t2, f2_pack(ex2(x0), ex2(x1)));
+            }
+            float ta, tb;
+            f2_unpack(t2, ta, tb);
+            tg[g] = ta + tb;
+            s += tg[g];
           }
           z = z * ex2(m - mn) + s;
           m = mn;
