@@ -40,7 +40,11 @@ using namespace sm100;
 
 constexpr int kBM = 128;         // query rows per tile (= TMEM lanes)
 constexpr int kBN = 128;         // keys per block
-constexpr int kWG = 4;                     // softmax warpgroups (32 key columns each)
+#ifndef DFS_ATTN_WG
+#define DFS_ATTN_WG 4
+#endif
+constexpr int kWG = DFS_ATTN_WG;           // softmax warpgroups splitting the 128 key columns
+constexpr int kCPT = 128 / kWG;            // key columns (logits) per softmax thread per block
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr uint32_t kTmemCols = 512;
@@ -365,19 +369,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++s_iter;
         continue;
 #endif
-        uint32_t sv[32];
-        tmem_ld32(tmem + lane_addr + sb * 128 + wg * 32, sv);
+        uint32_t sv[kCPT];
+#pragma unroll
+        for (int c = 0; c < kCPT / 32; ++c)
+          tmem_ld32(tmem + lane_addr + sb * 128 + wg * kCPT + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * c));
         tmem_wait_ld();
         // padded keys of a partial last block (attention.cpp:146-152); warp-uniform branch
-        const int valid = int(min(int64_t(kBN), p.nk - int64_t(vb) * kBN)) - wg * 32;
-        if (valid < 32) {
+        const int valid = int(min(int64_t(kBN), p.nk - int64_t(vb) * kBN)) - wg * kCPT;
+        if (valid < kCPT) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
+          for (int i = 0; i < kCPT; ++i)
             if (i >= valid) sv[i] = __float_as_uint(-INFINITY);
         }
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int i = 0; i < 32; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
+        for (int i = 0; i < kCPT; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         red_par[wg * kBM + r] = mx;
         named_bar_sync(kBarMax, kSoftmaxThreads);      // every slice loaded S and published its max
@@ -398,13 +404,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           lsum[1] = f2_mul(lsum[1], a2);
           m = m_new;
           const uint32_t o_addr = tmem + lane_addr + C::kOCol + wg * C::kOColsPerWG;
-          if constexpr (C::kOColsPerWG == 32) {
-            uint32_t ov[32];
-            tmem_ld32(o_addr, ov);
-            tmem_wait_ld();
+          if constexpr (C::kOColsPerWG >= 32) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st32(o_addr, ov);
+            for (int c = 0; c < C::kOColsPerWG; c += 32) {
+              uint32_t ov[32];
+              tmem_ld32(o_addr + c, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st32(o_addr + c, ov);
+            }
           } else {
             uint32_t ov[16];
             tmem_ld16(o_addr, ov);
@@ -416,9 +425,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // p = 2^(s*scale - m); every POLY-th pair on the FMA pipe (offloads MUFU)
         const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
-        uint32_t pk[16];
+        uint32_t pk[kCPT / 2];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < kCPT / 2; ++i) {
           float x0, x1;
           f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
           float p0, p1;
@@ -432,8 +441,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           lsum[i & 1] = f2_add(lsum[i & 1], f2_pack(p0, p1));
           pk[i] = pack_bf16(p0, p1);
         }
-        // P_j (bf16 pairs) over the first 64 columns of S[sb]: this slice's 32 keys -> 16 columns
-        tmem_st16(tmem + lane_addr + sb * 128 + wg * 16, pk);
+        // P_j (bf16 pairs) over the first 64 columns of S[sb]: this slice's kCPT keys -> kCPT/2 columns
+#pragma unroll
+        for (int c = 0; c < kCPT / 32; ++c)
+          tmem_st16(tmem + lane_addr + sb * 128 + wg * (kCPT / 2) + c * 16,
+                    *reinterpret_cast<const uint32_t(*)[16]>(pk + 16 * c));
         tmem_wait_st();
         tc_fence_before();
         if (tr) trace(p, 7 + (wg & 1) * 4, s_iter);
@@ -460,10 +472,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float inv_l = 1.f / l_tot;
       constexpr int kOC = C::kOColsPerWG;
       uint32_t ov[kOC];
-      if constexpr (kOC == 32)
-        tmem_ld32(tmem + lane_addr + C::kOCol + wg * kOC, *reinterpret_cast<uint32_t(*)[32]>(ov));
-      else
+      if constexpr (kOC >= 32) {
+#pragma unroll
+        for (int c = 0; c < kOC; c += 32)
+          tmem_ld32(tmem + lane_addr + C::kOCol + wg * kOC + c, *reinterpret_cast<uint32_t(*)[32]>(ov + c));
+      } else {
         tmem_ld16(tmem + lane_addr + C::kOCol + wg * kOC, *reinterpret_cast<uint32_t(*)[16]>(ov));
+      }
       tmem_wait_ld();
       tc_fence_before();
       if (i < p.nq) {
