@@ -243,7 +243,7 @@ def run_reference(args, wl):
     call_s, units_s, fixed_s, units = runs[len(runs) // 2]
     value = dense_flops / call_s / 1e12
     sample = rs.describe(call_s, units_s, fixed_s, units, reps=len(runs))
-    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+    out = {"metric": metric_for(args.workload), "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": call_s * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic iid normal (content does not change CPU op count)",
            "config": {"workload": wl["name"], "tokens": n, "heads": H, "d": d, "block": B, "sub_block": Bs,
