@@ -61,50 +61,84 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region: NVML every 10 ms
+    from a thread (nvidia-smi -lms as the fallback when NVML is unavailable)."""
+
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.stop = threading.Event()
         self.proc = None
+        self.thread = None
+
+    def _nvml_loop(self, nv, hdl):
+        bits = {nv.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                nv.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                nv.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                nv.nvmlClocksEventReasonSwPowerCap: "sw_power_cap"}
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hdl)
+                self.reasons.update(name for bit, name in bits.items() if r & bit)
+            except Exception:
+                pass
+            self.stop.wait(0.01)
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            hdl = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, hdl), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            pass
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread = threading.Thread(target=self._smi_read, daemon=True)
             self.thread.start()
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
+    def _smi_read(self):
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
+            parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
-                self.rows.append(parts)
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.max_mhz = float(parts[1])
+                except ValueError:
+                    continue
+                self.reasons.update(self.NAMES[i] for i in range(4) if parts[3 + i].lower() == "active")
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 def smooth_fields(dims, heads, d, seed, device, rounds=4):
@@ -346,7 +380,7 @@ def run_trajectory_bench(args, wl, dfs, dev, world, rank, local, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="HY", choices=sorted(WORKLOADS))
