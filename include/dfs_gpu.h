@@ -210,6 +210,10 @@ typedef struct {
   double* budget_out;    /* budget (1.0 when dense) */
   int* updated_out;      /* [H] mask_updated per head */
   double* sparsity_out;  /* [H] realized sparsity per head (metrics.cpp:39) */
+  /* [H] host, optional: attention recall of each head's mask on sparse steps
+   * (scheduler.cpp:129-131 record_recall), streamed without the N x N matrix, so
+   * it is available past the reference's 4096-row cap (dfs_block_recall). */
+  double* recall_out;
 } dfs_step_args;
 int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
 
@@ -240,6 +244,16 @@ int dfs_check_finite(const void* x, int64_t count, int dtype, int* nonfinite_hos
 /* attention.cpp:175-190 attention_recall -> *recall_host (synchronises). */
 int dfs_attention_recall(const float* scores, int64_t rows, int64_t cols, const uint8_t* bits, int64_t m,
                          int64_t block, double* recall_host, dfs_stream stream);
+
+/* attention.cpp:175-190 attention_recall(attention_scores(q, k), mask) for H
+ * heads at any N: sum |A o M| / sum |A| with A = row-softmax(q k^T / sqrt(d)),
+ * computed by streaming every key block through the tensor cores (no N x N
+ * storage). q, k: bf16 in `layout` (q_rows != NULL: q is raster NHD and logical
+ * row i is its row q_rows[i], as dfs_attn_args.in_rows); the mask is a CSR over
+ * (head, query block) with B = 128. recall_host [H] (synchronises). d in {64,128}. */
+int dfs_block_recall(dfs_handle* h, const void* q, const void* k, int layout, const uint32_t* q_rows,
+                     int64_t heads, int64_t n, int64_t d, const int32_t* blk_ptr, const int32_t* blk_idx,
+                     double* recall_host, dfs_stream stream);
 
 /* Per-handle kernel selection (A/B tests): route scoring / attention through
  * the geometry-generic kernels even where the tcgen05 ones apply. */

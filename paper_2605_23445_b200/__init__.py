@@ -10,6 +10,6 @@ from .ops import (  # noqa: F401
     apply_permutation, block3d_order, block_count_for, block_scores, block_sparse_attention, build_mask,
     default_handle, full_attention_output, hilbert2d_order, hilbert3d_order, invert_permutation, mean_pool,
     order_tokens, raster_order, realized_sparsity, run_step, should_update, sparse_attention_csr, topk_count,
-    topk_lut, topk_select, unpermute, validate_permutation)
+    topk_lut, topk_select, unpermute, validate_permutation, block_recall)
 
 LIBRARY = _capi.LIB_PATH

@@ -52,7 +52,8 @@ class StepArgs(C.Structure):
                 ("perm", _p), ("frames", _i64), ("height", _i64), ("width", _i64), ("block", _i64),
                 ("sub_block", _i64), ("layer", _i32), ("step", _i32), ("force_dense", _i32),
                 ("nonfinite", _p), ("dense_out", C.POINTER(_i32)), ("budget_out", C.POINTER(_dbl)),
-                ("updated_out", C.POINTER(_i32)), ("sparsity_out", C.POINTER(_dbl))]
+                ("updated_out", C.POINTER(_i32)), ("sparsity_out", C.POINTER(_dbl)),
+                ("recall_out", C.POINTER(_dbl))]
 
 
 _SIGS = {
@@ -86,6 +87,7 @@ _SIGS = {
     "dfs_aggregate_scores": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p]),
     "dfs_top_indices": (_i32, [_p, _i64, _i64, _i64, _p, _p]),
     "dfs_masked_scores": (_i32, [_p, _i64, _i64, _p, _i64, _i64, _p, _p]),
+    "dfs_block_recall": (_i32, [_p, _p, _p, _i32, _p, _i64, _i64, _i64, _p, _p, C.POINTER(_dbl), _p]),
     "dfs_check_finite": (_i32, [_p, _i64, _i32, C.POINTER(_i32), _p]),
     "dfs_attention_recall": (_i32, [_p, _i64, _i64, _p, _i64, _i64, C.POINTER(_dbl), _p]),
 }

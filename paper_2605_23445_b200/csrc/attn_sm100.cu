@@ -647,6 +647,14 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
 
 }  // namespace
 
+// bf16 token-tensor maps shared with the recall kernel (recall_sm100.cu)
+int make_token_map(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t heads, int64_t d) {
+  return make_map(map, base, layout, n, heads, d);
+}
+int make_row_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_t d) {
+  return make_gather_map(map, base, rows, d);
+}
+
 // [H, rows, d] fp16 operand map for the scorer (score_sm100.cu): box 64 x 128 x 1, SW128
 int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d) {
   EncodeFn enc = get_encode();

@@ -48,6 +48,10 @@ int lut_row_ptr_impl(int64_t heads, int64_t m, int64_t k, int32_t* blk_ptr, cuda
 int sparse_attn_generic(const dfs_attn_args& a, float scale, cudaStream_t stream);
 int sparse_attn_sm100(const dfs_attn_args& a, float scale, cudaStream_t stream);
 bool attn_sm100_supports(const dfs_attn_args& a);
+bool recall_sm100_supports(int64_t d);
+int block_recall_sm100(const void* q, const void* k, int layout, const uint32_t* q_rows, int64_t heads, int64_t n,
+                       int64_t d, const int32_t* blk_ptr, const int32_t* blk_idx, float* mass, double* recall,
+                       cudaStream_t stream);
 
 // ---- errors ----------------------------------------------------------------
 namespace {
@@ -137,11 +141,11 @@ struct dfs_handle {
   // workspaces
   Buf scratch_i32, flag;
   Buf k_hnd, v_hnd, pooled_q, pooled_k, scores, score_ws, lut, sel, counts;
-  Buf tmp_ptr, tmp_idx;
+  Buf tmp_ptr, tmp_idx, recall_ws;
   int64_t total_bytes() const {
     int64_t t = 0;
     for (const Buf* b : {&scratch_i32, &flag, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
-                         &lut, &sel, &counts, &tmp_ptr, &tmp_idx})
+                         &lut, &sel, &counts, &tmp_ptr, &tmp_idx, &recall_ws})
       t += int64_t(b->bytes);
     return t;
   }
@@ -631,6 +635,25 @@ int dfs_mask_cache_get(dfs_handle* h, int layer, int head, uint8_t* bits, int* l
   return DFS_OK;
 }
 
+// ------------------------------------------------------------- recall ------
+int dfs_block_recall(dfs_handle* h, const void* q, const void* k, int layout, const uint32_t* q_rows, int64_t heads,
+                     int64_t n, int64_t d, const int32_t* blk_ptr, const int32_t* blk_idx, double* recall_host,
+                     dfs_stream stream) {
+  if (int rc = check_handle(h)) return rc;
+  if (!q || !k || !blk_ptr || !blk_idx || !recall_host || heads < 1 || n < 1)
+    return fail(DFS_E_INVALID, "block_recall: bad arguments");
+  if (!recall_sm100_supports(d)) return fail(DFS_E_UNSUPPORTED, "block_recall: d must be 64 or 128");
+  cudaStream_t s = as_stream(stream);
+  if (int rc = h->recall_ws.ensure(sizeof(float) * size_t(heads * n) + sizeof(double) * size_t(heads) + 256))
+    return rc;
+  float* mass = h->recall_ws.as<float>();
+  double* rec = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(mass + heads * n) + 255) & ~uintptr_t(255));
+  if (int rc = block_recall_sm100(q, k, layout, q_rows, heads, n, d, blk_ptr, blk_idx, mass, rec, s)) return rc;
+  DFS_CUDA_CHECK(cudaMemcpyAsync(recall_host, rec, sizeof(double) * size_t(heads), cudaMemcpyDeviceToHost, s));
+  DFS_CUDA_CHECK(cudaStreamSynchronize(s));
+  return DFS_OK;
+}
+
 // ------------------------------------------------------------ run_step -----
 int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* a, dfs_stream stream) {
   if (int rc = check_handle(h)) return rc;
@@ -664,6 +687,8 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     if (int rc = attn_dispatch(h, at, s)) return rc;
     if (a->dense_out) *a->dense_out = 1;
     if (a->budget_out) *a->budget_out = 1.0;
+    if (a->recall_out)
+      for (int64_t hh = 0; hh < H; ++hh) a->recall_out[hh] = 1.0;  // StepStats{} default (scheduler.hpp:78-85)
     for (int64_t hh = 0; hh < H; ++hh) {
       if (a->updated_out) a->updated_out[hh] = 0;
       if (a->sparsity_out) a->sparsity_out[hh] = 0.0;
@@ -802,6 +827,11 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   at.out_rows = fwd;  // fused unpermute: row i -> raster row fwd[i] (scheduler.cpp:134)
   if ((rc = attn_dispatch(h, at, s))) return rc;
 
+  if (a->recall_out) {  // scheduler.cpp:129-131, without the N <= 4096 cap
+    if ((rc = dfs_block_recall(h, a->q, h->k_hnd.p, DFS_HND, fwd, H, n, d, L->ptr.as<int32_t>(),
+                               L->idx.as<int32_t>(), a->recall_out, stream)))
+      return rc;
+  }
   if (a->dense_out) *a->dense_out = 0;
   if (a->budget_out) *a->budget_out = budget;
   for (int64_t hh = 0; hh < H; ++hh) {

@@ -612,11 +612,12 @@ class StepStats:  # scheduler.hpp:78-85 (per head)
     budget: float = 1.0
     mask_updated: list = field(default_factory=list)
     sparsity: list = field(default_factory=list)
+    recall: list | None = None  # per head, when run_step(..., record_recall=True)
 
 
 def run_step(q, k, v, dims, params: ScoringParams, schedule: SparsitySchedule, cache: MaskCache, layer: int,
              step: int, force_dense: bool = False, perm: Permutation | None = None, out=None,
-             check_finite: bool = False):
+             check_finite: bool = False, record_recall: bool = False):
     """scheduler.hpp:93 run_step for ALL heads of one layer: q, k, v [N, H, d] bf16 raster order.
 
     Returns (out [N, H, d], StepStats)."""
@@ -634,16 +635,33 @@ def run_step(q, k, v, dims, params: ScoringParams, schedule: SparsitySchedule, c
     dense, budget = C.c_int(), C.c_double()
     upd = (C.c_int * h)()
     spars = (C.c_double * h)()
+    rec = (C.c_double * h)() if record_recall else None
     a = capi.StepArgs(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), n, h, d,
                       0 if perm is None else perm.forward.data_ptr(), dims.frames, dims.height, dims.width,
                       params.block_size, params.sub_block_size, layer, step, int(force_dense),
                       0 if flag is None else flag.data_ptr(), C.pointer(dense), C.pointer(budget),
-                      C.cast(upd, C.POINTER(C.c_int)), C.cast(spars, C.POINTER(C.c_double)))
+                      C.cast(upd, C.POINTER(C.c_int)), C.cast(spars, C.POINTER(C.c_double)),
+                      C.cast(rec, C.POINTER(C.c_double)) if rec is not None else None)
     capi.call("dfs_run_step", cache.handle.ptr, C.byref(schedule._s), C.byref(a), _stream())
     if flag is not None and int(flag.item()):
         raise ValueError("attention: non-finite input")
-    stats = StepStats(bool(dense.value), budget.value, [bool(x) for x in upd], list(spars))
+    stats = StepStats(bool(dense.value), budget.value, [bool(x) for x in upd], list(spars),
+                      list(rec) if rec is not None else None)
     return out, stats
+
+
+def block_recall(q, k, blk_ptr, blk_idx, layout=capi.DFS_HND, q_rows=None):
+    """attention_recall(attention_scores(q, k), mask) per head at any N (streamed, no N x N).
+
+    q, k: bf16 [H, N, d] (HND) or [N, H, d] (NHD); q_rows: q is raster NHD gathered by row."""
+    if q_rows is not None or layout == capi.DFS_NHD:
+        n, h, d = q.shape
+    else:
+        h, n, d = q.shape
+    rec = (C.c_double * h)()
+    capi.call("dfs_block_recall", default_handle().ptr, _ptr(q), _ptr(k), layout, _ptr(q_rows), h, n, d,
+              _ptr(blk_ptr), _ptr(blk_idx), C.cast(rec, C.POINTER(C.c_double)), _stream())
+    return list(rec)
 
 
 # --------------------------------------------------------------------------- #
