@@ -432,8 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
           float p0, p1;
           if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == POLY - 1) {
-            p0 = ex2_poly(x0);
-            p1 = ex2_poly(x1);
+            f2_unpack(ex2_poly2(x0, x1), p0, p1);
           } else {
             p0 = ex2(x0);
             p1 = ex2(x1);
@@ -589,7 +588,7 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
 // exp2 split between MUFU and the FMA-pipe polynomial: every POLY-th pair of a
 // thread's 32 logits goes to the polynomial (0 = all MUFU). DFS_ATTN_POLY
 // overrides the default for A/B measurements.
-constexpr int kDefaultPoly = 4;
+constexpr int kDefaultPoly = 3;
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
@@ -626,6 +625,8 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly;
   switch (poly) {
     case 0: rc = launch_kernel<D, 0>(mq, mk, mv, p, stream); break;
+    case 2: rc = launch_kernel<D, 2>(mq, mk, mv, p, stream); break;
+    case 3: rc = launch_kernel<D, 3>(mq, mk, mv, p, stream); break;
     case 8: rc = launch_kernel<D, 8>(mq, mk, mv, p, stream); break;
     default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
   }
