@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(128) attn_generic_kernel(dfs_attn_args a, int6
     if (active) {
       const int64_t orow = a.out_rows ? int64_t(a.out_rows[i]) : i;
       T* dst = o + row_offset(a.out_layout, a.nq, a.heads, d, h, orow);
-      const float inv = 1.f / l;
+      const float inv = l > 0.f ? 1.f / l : 0.f;  // empty key list -> zero row
 #pragma unroll
       for (int c = 0; c < DMAX; ++c)
         if (c < d) dst[c] = from_f32<T>(acc[c] * inv);
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(128) attn_f64_kernel(dfs_attn_args a, int64_t 
 #pragma unroll
   for (int t = 0; t < DPL; ++t) {
     const int64_t c = lane + 32 * t;
-    if (c < dv) dst[c] = float(acc[t]);
+    if (c < dv) dst[c] = z > 0.0 ? float(acc[t]) : 0.f;  // empty key list -> zero row
   }
 }
 

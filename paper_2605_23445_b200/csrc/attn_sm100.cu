@@ -468,7 +468,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int w = 0; w < kWG; ++w) l_tot += red_sum[w * kBM + r];
       const int64_t i = u * kBM + r;
-      const float inv_l = 1.f / l_tot;
+      // an empty key list (possible only through a caller-built CSR; the BlockMask entry
+      // points refuse it like attention.cpp:133-136) yields a zero row, never stale TMEM
+      const float inv_l = cnt > 0 ? 1.f / l_tot : 0.f;
       constexpr int kOC = C::kOColsPerWG;
       uint32_t ov[kOC];
       if constexpr (kOC >= 32) {
@@ -480,6 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_wait_ld();
       tc_fence_before();
+      if (cnt == 0) {
+#pragma unroll
+        for (int c = 0; c < kOC; ++c) ov[c] = 0u;
+      }
       if (i < p.nq) {
         const int64_t orow = p.out_rows ? int64_t(p.out_rows[i]) : i;
         __nv_bfloat16* dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;

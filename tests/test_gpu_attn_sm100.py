@@ -120,3 +120,26 @@ def test_sm100_hunyuan_two_heads_vs_oracle_rows():
         got = o[h].float().cpu().numpy()[rows]
         err = np.abs(got - ref[rows]).max() / np.abs(ref[rows]).max()
         assert err <= 2e-2, (h, err)
+
+
+@pytest.mark.parametrize("force_generic", [False, True])
+def test_empty_csr_row_gives_zero_output(force_generic):
+    """A caller-built CSR with an empty row (the BlockMask entry points refuse it, as
+    attention.cpp:133-136 does) must not leak stale accumulators: the row is zero."""
+    m = dfs()
+    h, n, d = 2, 640, 128
+    gen = torch.Generator().manual_seed(5)
+    q, k, v = (torch.randn(h, n, d, generator=gen).to(torch.bfloat16).cuda() for _ in range(3))
+    mq = n // 128
+    counts = torch.tensor([[2, 0, 1, 3, 2], [0, 1, 1, 1, 5]], dtype=torch.int32)
+    idx = []
+    for hh in range(h):
+        for u in range(mq):
+            idx.append(torch.arange(int(counts[hh, u]), dtype=torch.int32))
+    ptr = torch.zeros(h * mq + 1, dtype=torch.int32)
+    ptr[1:] = torch.cumsum(counts.reshape(-1), 0)
+    o = m.sparse_attention_csr(q, k, v, ptr.cuda(), torch.cat(idx).cuda(), 128, force_generic=force_generic)
+    torch.cuda.synchronize()
+    assert torch.isfinite(o.float()).all()
+    assert (o[0, 128:256].float() == 0).all() and (o[1, 0:128].float() == 0).all()
+    assert (o[0, 0:128].float().abs().sum() > 0)
