@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BIN = os.path.join(ROOT, "oracle", "_ref", "reftests")
-SUITES = ["test_curve", "test_attention", "test_mask_builder", "test_scheduler"]
+SUITES = ["test_curve", "test_attention", "test_mask_builder", "test_scheduler", "test_cli"]
 
 
 def _run(name, timeout=600):
@@ -42,3 +42,45 @@ def test_reference_unit_suite_passes_on_gpu_library(suite):
 def test_reference_acceptance_criteria_pass_on_gpu_library():
     r = _run("acceptance", timeout=1200)
     assert r.returncode == 0, (r.stdout[-4000:], r.stderr[-4000:])
+
+
+RUN_CONFIGS = {
+    # test_cli.cpp:36-52 small_run_config: 2 layers, updates at sparse steps 1, 3, 5
+    "small": {"seed": 3, "total_steps": 6, "warmup_fraction": 0.2, "phase_budgets": [0.5, 0.25],
+              "phase_fraction": 0.4, "update_interval": 2, "ordering": "hilbert3d", "block_size": 16,
+              "sub_block_size": 4, "dims": [4, 4, 4], "head_dim": 8, "layers": 2, "heads": 1,
+              "trajectory": {"smoothness": 2, "noise_start": 1.0, "noise_end": 0.0}},
+    # the reference defaults' schedule (T = 50, warmup 25 %, budgets 0.3/0.2/0.1, Delta = 12) on a
+    # 16^3 lattice with B = 64, B_s = 16, 2 layers x 2 heads, recall recorded (N = 4096 <= cap)
+    "schedule50": {"seed": 11, "total_steps": 50, "warmup_fraction": 0.25, "phase_budgets": [0.3, 0.2, 0.1],
+                   "phase_fraction": 0.25, "update_interval": 12, "ordering": "hilbert3d", "block_size": 64,
+                   "sub_block_size": 16, "dims": [16, 16, 16], "head_dim": 32, "layers": 2, "heads": 2,
+                   "trajectory": {"smoothness": 3, "noise_start": 1.5, "noise_end": 0.0}},
+}
+
+
+@pytest.mark.parametrize("name", sorted(RUN_CONFIGS))
+def test_cmd_run_outputs_byte_identical_to_reference(name, tmp_path):
+    """cmd_run (commands.cpp:221-319) end to end: the reference CLI code driving the
+    B200 library writes the same report.csv (step, layer, head, budget, sparsity,
+    recall at %.9g, mask_updated) and the same masks/*.dfsm files, byte for byte, as
+    the same code driving the reference's own CPU library."""
+    import json
+
+    cfg = tmp_path / "run.json"
+    cfg.write_text(json.dumps(RUN_CONFIGS[name]))
+    outs = {}
+    for tag in ("cmd_ref", "cmd_gpu"):
+        exe = os.path.join(BIN, tag)
+        if not os.path.exists(exe):
+            pytest.skip(f"{exe} not built (make -C oracle reftests needs /root/reference)")
+        out = tmp_path / tag
+        r = subprocess.run([exe, "run", str(cfg), str(out), "2"], capture_output=True, text=True, timeout=1200)
+        assert r.returncode == 0, (tag, r.stdout[-2000:], r.stderr[-2000:])
+        outs[tag] = out
+    ref, gpu = outs["cmd_ref"], outs["cmd_gpu"]
+    assert (ref / "report.csv").read_bytes() == (gpu / "report.csv").read_bytes()
+    ref_masks = sorted(p.name for p in (ref / "masks").iterdir())
+    assert ref_masks and ref_masks == sorted(p.name for p in (gpu / "masks").iterdir())
+    for fname in ref_masks:
+        assert (ref / "masks" / fname).read_bytes() == (gpu / "masks" / fname).read_bytes(), fname
