@@ -266,7 +266,12 @@ def run_reference(args, wl):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdfsref.so not built (needs "
                           "/root/reference at build time)"}))
         return
-    units_per_head = max(1, (rs.threads * args.ref_units_per_thread) // rs.heads_s)
+    # each step samples ~units_per_thread (head, query-block) units per host thread; by default
+    # sized so the whole --warmup + --steps run stays near 2.5 minutes (~0.6 s per unit per thread)
+    upt = args.ref_units_per_thread
+    if upt <= 0:
+        upt = max(1, int(150.0 / max(1, args.warmup + args.steps) / 0.6))
+    units_per_head = max(1, (rs.threads * upt) // rs.heads_s)
     runs = []
     for i in range(args.warmup + args.steps):
         r = rs.run(units_per_head)
@@ -385,7 +390,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="HY", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-units-per-thread", type=int, default=20)
+    ap.add_argument("--ref-units-per-thread", type=int, default=0,
+                    help="reference arm sample size per step (0: sized for a ~2.5 min run)")
     ap.add_argument("--profile", action="store_true", help="only run warmup+steps of the step (for ncu)")
     ap.add_argument("--trajectory", action="store_true",
                     help="diffusion trajectory: T=50 steps, 25%% dense warmup, phase budgets, mask update every "
