@@ -57,9 +57,25 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
                                                       float* __restrict__ pooled, int64_t pool,
                                                       int32_t* __restrict__ nonfinite) {
   constexpr int V = Vec<T>::N;
+  constexpr int kBatch = 8;  // independent 16-byte row loads in flight per thread
   const int64_t vec_per_row = d / V;
   const int64_t slots = heads * vec_per_row;
   const int64_t r0 = int64_t(blockIdx.x) * rows;
+  // the CTA's row indices once in shared memory (rows <= 64): the per-row loads of the
+  // slots below then have no dependent index load in front of them
+  __shared__ int64_t s_src[64], s_dst[64];
+  for (int t = threadIdx.x; t < rows; t += blockDim.x) {  // blockDim may be < rows for narrow rows
+    const int64_t i = r0 + t;
+    int64_t si = -1, di = -1;
+    if (i < n) {
+      si = kScatter ? i : int64_t(idx[i]);
+      di = kScatter ? int64_t(idx[i]) : i;
+      if (si >= n || di >= n) si = di = -1;  // invalid permutation entry: no wild access
+    }
+    s_src[t] = si;
+    s_dst[t] = di;
+  }
+  __syncthreads();
   bool bad = false;
   for (int64_t s = threadIdx.x; s < slots; s += blockDim.x) {
     const int64_t h = s / vec_per_row;
@@ -69,23 +85,28 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = 0.0;
     }
-#pragma unroll 8
-    for (int r = 0; r < rows; ++r) {
-      const int64_t i = r0 + r;
-      if (i >= n) break;
-      // gather: read source row idx[i] -> write dest row i; scatter: the reverse
-      const int64_t si = kScatter ? i : int64_t(idx[i]);
-      const int64_t di = kScatter ? int64_t(idx[i]) : i;
-      if (si >= n || di >= n) continue;  // invalid permutation entry: no wild access
-      const uint4 u = *reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c);
-      if (dst) *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) = u;
-      if (kPool || nonfinite) {
-        float x[V];
-        unpack<T>(u, x);
+    for (int rb = 0; rb < rows; rb += kBatch) {
+      uint4 u[kBatch];
 #pragma unroll
-        for (int j = 0; j < V; ++j) {
-          if (kPool) acc[j] += double(x[j]);
-          bad |= !isfinite(x[j]);
+      for (int k = 0; k < kBatch; ++k) {
+        const int64_t si = rb + k < rows ? s_src[rb + k] : -1;
+        u[k] = si >= 0 ? __ldg(reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c))
+                       : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        if (rb + k >= rows) break;
+        const int64_t di = s_dst[rb + k];
+        if (di < 0) continue;
+        if (dst) *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) = u[k];
+        if (kPool || nonfinite) {
+          float x[V];
+          unpack<T>(u[k], x);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            if (kPool) acc[j] += double(x[j]);
+            bad |= !isfinite(x[j]);
+          }
         }
       }
     }
@@ -137,6 +158,7 @@ int launch(const void* src, int src_layout, void* dst, int dst_layout, const uin
   // dst == NULL: read-only pass (pooled rows and/or the finite check of a gathered order)
   const bool vec_ok = d % Vec<T>::N == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
                       (reinterpret_cast<uintptr_t>(dst) & 15) == 0 && (!pooled || pool <= 64);
+  // (rows per CTA: the pooling group, or 16; both <= 64 as the kernel's index cache requires)
   const int64_t rows = pooled ? pool : 16;
   const int64_t grid = ceil_div(n, rows);
   if (grid > int64_t(INT32_MAX)) return fail(DFS_E_UNSUPPORTED, "permute: too many rows");
