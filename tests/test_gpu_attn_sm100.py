@@ -186,3 +186,35 @@ def test_fuzz_tcgen05_vs_fp32_torch_reference():
         for name, o in (("tcgen05", o_fast), ("simt", o_slow)):
             err = float((o.float() - ref).abs().max() / ref.abs().max())
             assert err <= 2e-2, (trial, name, n, h, d, k, gather, err)
+
+
+@pytest.mark.parametrize("jump", [0.5, 40.0, 400.0])
+def test_logit_jump_across_blocks(jump):
+    """Online-softmax rescaling under large row-max jumps: key block 3 carries logits
+    `jump` log2 units above block 0's (400 would overflow fp32 without the O/l rescale,
+    0.5 stays under the lazy-rescale threshold). Output must match a torch fp32 softmax,
+    and a following ordinary call must be unaffected."""
+    m = dfs()
+    gen = torch.Generator().manual_seed(7)
+    h, n, d = 2, 1024 + 40, 128
+    q = torch.full((h, n, d), 1.0) + 0.05 * torch.randn(h, n, d, generator=gen)
+    kk = 0.05 * torch.randn(h, n, d, generator=gen)
+    # logit_log2 = q.k / sqrt(d) * log2(e): choose block 3's key scale for the requested jump
+    c = jump / (d / d ** 0.5 * 1.4426950408889634)
+    kk[:, 3 * 128:4 * 128] += c
+    v = torch.randn(h, n, d, generator=gen)
+    q, kk, v = (x.to(torch.bfloat16).cuda() for x in (q, kk, v))
+    mq = -(-n // 128)
+    lut = torch.arange(mq, dtype=torch.int32).repeat(h, mq, 1).cuda()
+    ptr = m.ops.lut_row_ptr(h, mq, mq)
+    for _ in range(2):
+        o = m.sparse_attention_csr(q, kk, v, ptr, lut.reshape(-1), 128, layout=1, out_layout=1)
+        torch.cuda.synchronize()
+        ref = torch.softmax(q.float() @ kk.float().transpose(1, 2) / d ** 0.5, -1) @ v.float()
+        assert torch.isfinite(o.float()).all()
+        assert rel(o.float(), ref) <= 2e-2, rel(o.float(), ref)
+    # an ordinary call after the recovery pass
+    q2, k2, v2 = (torch.randn(h, n, d, generator=gen).to(torch.bfloat16).cuda() for _ in range(3))
+    o2 = m.sparse_attention_csr(q2, k2, v2, ptr, lut.reshape(-1), 128, layout=1, out_layout=1)
+    ref2 = torch.softmax(q2.float() @ k2.float().transpose(1, 2) / d ** 0.5, -1) @ v2.float()
+    assert rel(o2.float(), ref2) <= 2e-2
