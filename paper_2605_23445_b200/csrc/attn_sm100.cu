@@ -662,13 +662,13 @@ int make_row_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_
   return make_gather_map(map, base, rows, d);
 }
 
-// [H, rows, d] fp16 operand map for the scorer (score_sm100.cu): box 64 x 128 x 1, SW128
-int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d) {
+// [H, rows, d] fp16 operand map for the scorer (score_sm100.cu): box 64 x box_rows x 1, SW128
+int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d, int box_rows) {
   EncodeFn enc = get_encode();
   if (!enc) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {cuuint64_t(d), cuuint64_t(rows), cuuint64_t(heads)};
   cuuint64_t strides[2] = {cuuint64_t(d) * 2, cuuint64_t(rows) * cuuint64_t(d) * 2};
-  cuuint32_t box[3] = {64, 128, 1}, estr[3] = {1, 1, 1};
+  cuuint32_t box[3] = {64, cuuint32_t(box_rows), 1}, estr[3] = {1, 1, 1};
   const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -22,12 +22,14 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
 namespace dfsgpu {
 
-int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d);
+int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d, int box_rows = 128);
 
 namespace {
 
@@ -41,24 +43,32 @@ constexpr int kThreads = 64 + kSoftThreads;
 constexpr float kLoScale = 2048.f;        // 2^11
 constexpr float kInvLoScale = 1.f / 2048.f;
 
+// CTA pairs (cta_group::2): the pair's MMA is M = 256 (each CTA's own 128-row stripe)
+// x N = 128 keys, and each CTA holds only half of every key tile (64 keys) — the pooled
+// key operand is read from L2 once per pair instead of once per CTA. The K stream is the
+// kernel's L2->SM traffic bound (~5.3 GB per HY call unpaired).
 template <int D>
 struct SCfg {
   static constexpr int kChunks = D / 64;
-  static constexpr int kChunkBytes = 128 * 128;          // 128 rows x 64 fp16
-  static constexpr int kOpBytes = kRows * D * 2;          // one hi or lo operand tile
-  static constexpr int kStages = D == 64 ? 4 : 2;
+  static constexpr int kChunkBytes = 128 * 128;          // A: 128 rows x 64 fp16
+  static constexpr int kOpBytes = kRows * D * 2;          // one hi or lo Q stripe
+  static constexpr int kHalfKeys = kKeys / 2;             // key rows this CTA supplies
+  static constexpr int kBChunkBytes = kHalfKeys * 128;    // B: 64 rows x 64 fp16
+  static constexpr int kHalfBytes = kHalfKeys * D * 2;    // one hi or lo key half-tile
+  static constexpr int kStages = D == 64 ? 8 : 4;
   static constexpr int kQOff = 0;                         // Qhi, Qlo
-  static constexpr int kKOff = 2 * kOpBytes;              // stages x (Khi, Klo)
-  static constexpr int kRedOff = kKOff + kStages * 2 * kOpBytes;  // float m[kSWG][128], z[kSWG][128]
-  static constexpr int kBarOff = kRedOff + 2 * kSWG * kRows * 4;
+  static constexpr int kKOff = 2 * kOpBytes;              // stages x (Khi, Klo) halves
+  static constexpr int kRedOff = kKOff + kStages * 2 * kHalfBytes;  // float [2][m | z][kSWG][128]
+  static constexpr int kBarOff = kRedOff + 2 * 2 * kSWG * kRows * 4;
   static constexpr int kSmem = kBarOff + 256 + 1024;
 };
 
-// kind::f16 with fp16 inputs (formats 0), fp32 accumulation, K-major A and B
-constexpr uint32_t kIdesc = (1u << 4) | (uint32_t(kKeys >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
+// kind::f16 with fp16 inputs (formats 0), fp32 accumulation, K-major A and B, M = 256 (pair)
+constexpr uint32_t kIdesc = (1u << 4) | (uint32_t(kKeys >> 3) << 17) | (uint32_t(2 * kRows >> 4) << 24);
 
 struct SParams {
-  int64_t heads, qvalid, kvalid, m, subs, nrt, nkt, items;
+  int64_t heads, qvalid, kvalid, m, subs, nrt, nkt;
+  int64_t npr, pitems;  // stripe pairs per head (stripes 2i, 2i+1), pairs in total
   const float* fac;   // [H]: scale_log2 / (sq * sk)
   double* S;
   float* tsum;        // per-CTA scratch [gridDim][m][128]: unnormalised row tile sums
@@ -67,7 +77,7 @@ struct SParams {
 
 struct SBars {
   uint64_t q_full, q_empty;
-  uint64_t k_full[4], k_empty[4];
+  uint64_t k_full[8], k_empty[8];
   uint64_t acc_full[2], acc_free[2];
   uint32_t tmem_base;
 };
@@ -81,7 +91,7 @@ struct SBars {
 // L2 (it is re-read right after it is written), so the second GEMM + exp pass of a
 // two-pass softmax is replaced by one L2 round trip of 4 bytes per (row, block).
 template <int D, int SUBS>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     score_sm100_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
                        const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
                        const SParams p) {
@@ -90,6 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   SBars* bars = reinterpret_cast<SBars*>(smem + C::kBarOff);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();             // 0: leader (issues the pair's MMAs)
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
     mbar_init(&bars->q_empty, 1);
@@ -99,40 +111,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->acc_full[i], 1);
-      mbar_init(&bars->acc_free[i], kSoftThreads / 32);  // one arrive per softmax warp
+      mbar_init(&bars->acc_free[i], 2 * kSoftThreads / 32);  // one arrive per softmax warp of the pair
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  cluster_sync();  // the peer's barriers exist before any remote arrive or TMA signal
+  if (warp == 1) tmem_alloc_pair<512>(&bars->tmem_base);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
   if (warp == 0) {
     // ============ TMA producer (warp-uniform loop, one elected lane issues) ============
+    // Both CTAs load their own Q stripe and their half of each key tile; the bytes are
+    // counted on the leader's barriers (the leader posts the pair's expected total).
     uint32_t q_phase = 0, ring = 0;
-    for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
-      const int h = int(it / p.nrt), rt = int(it % p.nrt);
+    for (int64_t pit = cid; pit < p.pitems; pit += ncl) {
+      const int h = int(pit / p.npr), rt = int(pit % p.npr) * 2 + int(rank);
       mbar_wait(&bars->q_empty, q_phase ^ 1);
       q_phase ^= 1;
       if (elect_one()) {
-        mbar_expect_tx(&bars->q_full, 2 * C::kOpBytes);
+        if (rank == 0) mbar_expect_tx(&bars->q_full, 2 * 2 * C::kOpBytes);
         for (int c = 0; c < C::kChunks; ++c) {
-          tma_load_3d(smem + C::kQOff + c * C::kChunkBytes, &tm_qh, &bars->q_full, c * 64, rt * kRows, h);
-          tma_load_3d(smem + C::kQOff + C::kOpBytes + c * C::kChunkBytes, &tm_ql, &bars->q_full, c * 64, rt * kRows, h);
+          tma_load_3d_pair(smem + C::kQOff + c * C::kChunkBytes, &tm_qh, &bars->q_full, c * 64, rt * kRows, h);
+          tma_load_3d_pair(smem + C::kQOff + C::kOpBytes + c * C::kChunkBytes, &tm_ql, &bars->q_full, c * 64,
+                           rt * kRows, h);
         }
       }
       __syncwarp();
       for (int kt = 0; kt < p.nkt; ++kt) {
         const uint32_t slot = ring % C::kStages;
         mbar_wait(&bars->k_empty[slot], ((ring / C::kStages) & 1) ^ 1);
+#ifdef DFS_SCORE_SKIP_TMA  // experiment builds only: key tiles never loaded (garbage operands)
+        if (elect_one() && rank == 0) mbar_arrive(&bars->k_full[slot]);
+        __syncwarp();
+        ++ring;
+        continue;
+#endif
         if (elect_one()) {
-          mbar_expect_tx(&bars->k_full[slot], 2 * C::kOpBytes);
-          uint8_t* dst = smem + C::kKOff + slot * 2 * C::kOpBytes;
+          if (rank == 0) mbar_expect_tx(&bars->k_full[slot], 2 * 2 * C::kHalfBytes);
+          uint8_t* dst = smem + C::kKOff + slot * 2 * C::kHalfBytes;
+          const int k0 = kt * kKeys + int(rank) * C::kHalfKeys;
           for (int c = 0; c < C::kChunks; ++c) {
-            tma_load_3d(dst + c * C::kChunkBytes, &tm_kh, &bars->k_full[slot], c * 64, kt * kKeys, h);
-            tma_load_3d(dst + C::kOpBytes + c * C::kChunkBytes, &tm_kl, &bars->k_full[slot], c * 64, kt * kKeys, h);
+            tma_load_3d_pair(dst + c * C::kBChunkBytes, &tm_kh, &bars->k_full[slot], c * 64, k0, h);
+            tma_load_3d_pair(dst + C::kHalfBytes + c * C::kBChunkBytes, &tm_kl, &bars->k_full[slot], c * 64, k0, h);
           }
         }
         __syncwarp();
@@ -140,38 +163,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ============ MMA issuer: D1 = Qhi Khi^T, D2 = Qhi Klo^T + Qlo Khi^T ============
-    uint32_t q_phase = 0, ring = 0, acc_iter = 0;
-    constexpr uint32_t kHi = desc_sw128_hi(1024);
-    const uint32_t qh_lo = desc_sw128_lo(smem_u32(smem + C::kQOff), 16);
-    const uint32_t ql_lo = qh_lo + (C::kOpBytes >> 4);
-    const uint32_t k_lo0 = desc_sw128_lo(smem_u32(smem + C::kKOff), 16);
-    for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
-      mbar_wait(&bars->q_full, q_phase);
-      q_phase ^= 1;
-      for (int kt = 0; kt < p.nkt; ++kt) {
-        const uint32_t slot = ring % C::kStages;
-        mbar_wait(&bars->k_full[slot], (ring / C::kStages) & 1);
-        ++ring;
-        const uint32_t b = acc_iter & 1;
-        mbar_wait(&bars->acc_free[b], ((acc_iter >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t kh_lo = k_lo0 + slot * ((2 * C::kOpBytes) >> 4), kl_lo = kh_lo + (C::kOpBytes >> 4);
-        const uint32_t d1 = tmem + b * 256, d2 = d1 + 128;
-        if (elect_one()) {
+    // ============ MMA issuer (leader only): D1 = Qhi Khi^T, D2 = Qhi Klo^T + Qlo Khi^T ============
+    if (rank == 0) {
+      uint32_t q_phase = 0, ring = 0, acc_iter = 0;
+      constexpr uint32_t kHi = desc_sw128_hi(1024);
+      const uint32_t qh_lo = desc_sw128_lo(smem_u32(smem + C::kQOff), 16);
+      const uint32_t ql_lo = qh_lo + (C::kOpBytes >> 4);
+      const uint32_t k_lo0 = desc_sw128_lo(smem_u32(smem + C::kKOff), 16);
+      for (int64_t pit = cid; pit < p.pitems; pit += ncl) {
+        mbar_wait(&bars->q_full, q_phase);
+        q_phase ^= 1;
+        for (int kt = 0; kt < p.nkt; ++kt) {
+          const uint32_t slot = ring % C::kStages;
+          mbar_wait(&bars->k_full[slot], (ring / C::kStages) & 1);
+          ++ring;
+          const uint32_t b = acc_iter & 1;
+          mbar_wait(&bars->acc_free[b], ((acc_iter >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t kh_lo = k_lo0 + slot * ((2 * C::kHalfBytes) >> 4), kl_lo = kh_lo + (C::kHalfBytes >> 4);
+          const uint32_t d1 = tmem + b * 256, d2 = d1 + 128;
+          if (elect_one()) {
 #pragma unroll
-          for (int s = 0; s < D / 16; ++s) {
-            const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
-            umma_ss(d1, qh_lo + off, kHi, kh_lo + off, kHi, kIdesc, s > 0);
-            umma_ss(d2, qh_lo + off, kHi, kl_lo + off, kHi, kIdesc, s > 0);
-            umma_ss(d2, ql_lo + off, kHi, kh_lo + off, kHi, kIdesc, 1);
+            for (int s = 0; s < D / 16; ++s) {
+              const uint32_t oa = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
+              const uint32_t ob = ((s >> 2) * C::kBChunkBytes + (s & 3) * 32) >> 4;
+#ifndef DFS_SCORE_SKIP_MMA  // experiment builds only: isolate the softmax / TMA side
+              umma_ss_pair(d1, qh_lo + oa, kHi, kh_lo + ob, kHi, kIdesc, s > 0);
+              umma_ss_pair(d2, qh_lo + oa, kHi, kl_lo + ob, kHi, kIdesc, s > 0);
+              umma_ss_pair(d2, ql_lo + oa, kHi, kh_lo + ob, kHi, kIdesc, 1);
+#endif
+            }
+            umma_commit_pair(&bars->k_empty[slot]);
+            umma_commit_pair(&bars->acc_full[b]);
+            if (kt == p.nkt - 1) umma_commit_pair(&bars->q_empty);
           }
-          umma_commit(&bars->k_empty[slot]);
-          umma_commit(&bars->acc_full[b]);
-          if (kt == p.nkt - 1) umma_commit(&bars->q_empty);
+          __syncwarp();
+          ++acc_iter;
         }
-        __syncwarp();
-        ++acc_iter;
       }
     }
   } else {
@@ -180,27 +208,79 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 2) >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
-    float* red_m = reinterpret_cast<float*>(smem + C::kRedOff);
-    float* red_z = red_m + kSWG * kRows;
+    float* red = reinterpret_cast<float*>(smem + C::kRedOff);  // [stripe parity][m | z][kSWG][kRows]
     float* tsum = p.tsum + int64_t(blockIdx.x) * p.m * kRows;            // [v][row]
     float* tmax = p.tmax + int64_t(blockIdx.x) * p.nkt * kSWG * kRows;   // [kt][slice][row]
     constexpr int G = 32 / SUBS;                                           // key blocks per slice per tile
-    uint32_t acc_iter = 0;
-    for (int64_t it = blockIdx.x; it < p.items; it += gridDim.x) {
-      const int h = int(it / p.nrt), rt = int(it % p.nrt);
+    const int m32 = int(p.m), kvalid32 = int(p.kvalid);                    // (host checks < 2^31 / 128)
+    // The fix-up of stripe s runs inside stripe s+1: at tile kt a thread first reads the
+    // scratch entries its own slice wrote for tile kt of stripe s (program order: no
+    // barrier), turns them into probabilities with stripe s's merged row statistics and
+    // then overwrites them. The tensor pipe therefore never idles for a fix-up phase;
+    // only the CTA's last stripe is fixed up after the loop.
+    struct Prev {
+      bool valid = false;
+      int64_t h = 0;
+      int u = 0;               // S row block of this thread's pooled row in the previous stripe
+      float mm = 0.f, inv_z = 0.f;
+    } prev;
+    // probabilities of (row, key blocks of slice wg in tile kt) for the previous stripe;
+    // every lane of the warp takes part (sub-row sums by shuffles)
+    auto fix_tile = [&](int kt, const float (&t)[G], float mu) {
+      const float e = ex2(mu - prev.mm);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int v = kt * (kKeys / SUBS) + wg * G + g;
+        float pr = t[g] > 0.f ? t[g] * e * prev.inv_z : 0.f;
+#pragma unroll
+        for (int o = 1; o < SUBS; o <<= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+        // S is write-once output: streaming stores keep it from evicting the L2-resident scratch
+        if ((lane % SUBS) == 0 && prev.u < m32 && v < m32)
+          __stcs(p.S + (prev.h * p.m + prev.u) * p.m + v, double(pr));
+      }
+    };
+    auto load_tile = [&](int kt, float (&t)[G], float& mu) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int v = kt * (kKeys / SUBS) + wg * G + g;
+        t[g] = v < m32 ? tsum[v * kRows + r] : 0.f;
+      }
+      mu = tmax[(kt * kSWG + wg) * kRows + r];
+    };
+    uint32_t acc_iter = 0, parity = 0;
+    for (int64_t pit = cid; pit < p.pitems; pit += ncl) {
+      const int h = int(pit / p.npr), rt = int(pit % p.npr) * 2 + int(rank);
       const float f = p.fac[h];
+      const uint64_t f2 = f2_pack(f, f), g2 = f2_pack(f * kInvLoScale, f * kInvLoScale);
       const int64_t row = int64_t(rt) * kRows + r;     // pooled query row
       float m = -INFINITY, z = 0.f;
-      for (int kt = 0; kt < p.nkt; ++kt) {
+      // the previous stripe's scratch entries, fetched one tile ahead (L2 latency hidden
+      // behind a whole tile of work)
+      float t_nx[G], mu_nx = 0.f;
+      if (prev.valid) load_tile(0, t_nx, mu_nx);
+      // one key tile; kMask only for the last tile (the one holding the end of the valid
+      // keys) — a runtime test here is if-converted into per-element selects every tile
+      auto tile = [&](int kt, auto mask_tag) {
+        constexpr bool kMask = decltype(mask_tag)::value;
+        float t_old[G], mu_old = mu_nx;
+#pragma unroll
+        for (int g = 0; g < G; ++g) t_old[g] = t_nx[g];
+        if (prev.valid && kt + 1 < p.nkt) load_tile(kt + 1, t_nx, mu_nx);
         const uint32_t b = acc_iter & 1;
         mbar_wait(&bars->acc_full[b], (acc_iter >> 1) & 1);
         tc_fence_after();
-        const int64_t cbase = int64_t(kt) * kKeys + wg * 32;
+#ifdef DFS_SCORE_SKIP_SOFTMAX  // experiment builds only (tools/score_exp.sh): isolate the MMA/TMA side
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&bars->acc_free[b], 0);
+        ++acc_iter;
+        return;
+#endif
+        const int cbase = kt * kKeys + wg * 32;
         // logits l = (D1 + D2 / 2^11) * f in packed fp32x2 arithmetic; only the tile holding
         // the end of the valid pooled keys masks (warp-uniform branch)
         uint64_t l2[16];
         {
-          const uint64_t f2 = f2_pack(f, f), g2 = f2_pack(f * kInvLoScale, f * kInvLoScale);
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             uint32_t a1[16], a2[16];
@@ -215,15 +295,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->acc_free[b]);
+        if (lane == 0) mbar_arrive_cluster(&bars->acc_free[b], 0);  // the leader's barrier
         ++acc_iter;
-        if (cbase + 32 > p.kvalid) {
+        const int rem = kvalid32 - cbase;
+        if (kMask && rem < 32) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x0, x1;
             f2_unpack(l2[i], x0, x1);
-            if (cbase + 2 * i >= p.kvalid) x0 = -INFINITY;
-            if (cbase + 2 * i + 1 >= p.kvalid) x1 = -INFINITY;
+            if (2 * i >= rem) x0 = -INFINITY;
+            if (2 * i + 1 >= rem) x1 = -INFINITY;
             l2[i] = f2_pack(x0, x1);
           }
         }
@@ -259,18 +340,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int g = 0; g < G; ++g) tg[g] = 0.f;
         }
+        if (prev.valid) fix_tile(kt, t_old, mu_old);
         // coalesced across the warp: 32 consecutive rows per (v) / (kt, slice) entry
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const int64_t v = (cbase + g * SUBS) / SUBS;
-          if (v < p.m) tsum[v * kRows + r] = tg[g];
+          const int v = (cbase + g * SUBS) / SUBS;
+          if (v < m32) tsum[v * kRows + r] = tg[g];
         }
-        tmax[(int64_t(kt) * kSWG + wg) * kRows + r] = m;
-      }
-      // merge the slices' (max, sum) of this row
+        tmax[(kt * kSWG + wg) * kRows + r] = m;
+      };
+      for (int kt = 0; kt + 1 < p.nkt; ++kt) tile(kt, std::false_type{});
+      tile(int(p.nkt) - 1, std::true_type{});
+      // merge the slices' (max, sum) of this row (slots double-buffered by stripe parity)
+      float* red_m = red + parity * 2 * kSWG * kRows;
+      float* red_z = red_m + kSWG * kRows;
       red_m[wg * kRows + r] = m;
       red_z[wg * kRows + r] = z;
-      named_bar_sync(1, kSoftThreads);  // also orders the tsum/tmax stores before the fix-up reads
+      named_bar_sync(1, kSoftThreads);
       float mm = -INFINITY;
 #pragma unroll
       for (int w = 0; w < kSWG; ++w) mm = fmaxf(mm, red_m[w * kRows + r]);
@@ -280,37 +366,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mw = red_m[w * kRows + r];
         if (mw > -INFINITY) zz += red_z[w * kRows + r] * ex2(mw - mm);
       }
-      const float inv_z = 1.f / zz;
-      // fix-up: probabilities (fp32, attention.cpp:120) summed over SUBS sub-rows, fp64 S;
-      // warpgroup wg takes every kSWG-th key block
-      const int64_t u = row / SUBS;
-      constexpr int kU = 8;  // independent L2 loads in flight per thread
-      for (int64_t v0 = wg; v0 < p.m; v0 += kSWG * kU) {
-        float t[kU], mu[kU];
-#pragma unroll
-        for (int i = 0; i < kU; ++i) {
-          const int64_t v = v0 + int64_t(i) * kSWG;
-          const int64_t col = v * SUBS;
-          const int kt = int(col / kKeys), sl = int((col % kKeys) / 32);
-          t[i] = v < p.m ? tsum[v * kRows + r] : 0.f;
-          mu[i] = v < p.m ? tmax[(int64_t(kt) * kSWG + sl) * kRows + r] : 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < kU; ++i) {
-          const int64_t v = v0 + int64_t(i) * kSWG;
-          float pr = t[i] > 0.f ? t[i] * ex2(mu[i] - mm) * inv_z : 0.f;
-#pragma unroll
-          for (int o = 1; o < SUBS; o <<= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
-          if ((lane % SUBS) == 0 && u < p.m && v < p.m) p.S[(int64_t(h) * p.m + u) * p.m + v] = double(pr);
-        }
+      prev.valid = true;
+      prev.h = h;
+      prev.u = int(row / SUBS);
+      prev.mm = mm;
+      prev.inv_z = 1.f / zz;
+      parity ^= 1;
+    }
+    // the CTA's last stripe: fix-up without a following stripe to hide it in
+    if (prev.valid) {
+      for (int kt = 0; kt < p.nkt; ++kt) {
+        float t_old[G], mu_old;
+        load_tile(kt, t_old, mu_old);
+        fix_tile(kt, t_old, mu_old);
       }
-      named_bar_sync(1, kSoftThreads);  // slots and scratch are rewritten by the next stripe
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // every MMA of the pair has completed and been consumed
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == 1) tmem_dealloc_pair<512>(tmem);
 }
 
 // ---- operand preparation: per-head power-of-two scale, fp16 hi/lo split ----------
@@ -360,7 +435,7 @@ int launch(const CUtensorMap* maps, const SParams& p, cudaStream_t stream) {
                                         C::kSmem));
     attr = true;
   }
-  const int64_t grid = p.items < kNumSMs ? p.items : kNumSMs;
+  const int64_t grid = 2 * p.pitems < kNumSMs ? 2 * p.pitems : kNumSMs;  // whole pairs (kNumSMs is even)
   score_sm100_kernel<D, SUBS><<<unsigned(grid), kThreads, C::kSmem, stream>>>(maps[0], maps[1], maps[2], maps[3], p);
   DFS_LAUNCH_CHECK("score_sm100");
   return DFS_OK;
@@ -414,7 +489,7 @@ int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t 
   CUtensorMap maps[4];
   int rc;
   if ((rc = make_map_f16(&maps[0], qh, valid, heads, d)) || (rc = make_map_f16(&maps[1], ql, valid, heads, d)) ||
-      (rc = make_map_f16(&maps[2], kh, valid, heads, d)) || (rc = make_map_f16(&maps[3], kl, valid, heads, d)))
+      (rc = make_map_f16(&maps[2], kh, valid, heads, d, 64)) || (rc = make_map_f16(&maps[3], kl, valid, heads, d, 64)))
     return rc;
   SParams p;
   p.heads = heads;
@@ -424,7 +499,8 @@ int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t 
   p.subs = block / sub_block;
   p.nrt = ceil_div(p.m * p.subs, kRows);
   p.nkt = ceil_div(valid, kKeys);
-  p.items = heads * p.nrt;
+  p.npr = ceil_div(p.nrt, int64_t(2));
+  p.pitems = heads * p.npr;
   p.fac = fac;
   p.S = S;
   p.tsum = tsum;
