@@ -12,11 +12,13 @@
 // three fp16 UMMAs at the full 16-bit tensor rate (twice TF32's), fp32
 // accumulation in TMEM: D1 = hi*hi, D2 = the two cross terms.
 //
-// One CTA per (head, 128 pooled query rows); two passes over the 128-wide
-// pooled key tiles: pass 0 the row max / partition function, pass 1 the fp32
-// probabilities summed over `subs` columns in registers and over `subs` rows
-// with warp shuffles, written as fp64 S entries. Warp roles as in K5: warp 0
-// TMA, warp 1 MMA issue, warps 2-5 one pooled row per thread (= TMEM lane).
+// CTA pairs (cta_group::2, cluster of 2): each CTA owns a 128-row stripe of pooled
+// queries; the leader issues M = 256 MMAs over both stripes while each CTA loads only
+// half of every 128-key tile. One pass over the key tiles: each softmax slice (32 key
+// columns) keeps an exact online (max, sum) and writes unnormalised sub-row tile sums
+// to an L2-resident per-CTA scratch; the fix-up that turns them into probabilities
+// (summed over `subs` rows by shuffles, fp64 S) runs inside the NEXT stripe's tile loop.
+// Warp roles as in K5: warp 0 TMA, warp 1 MMA issue (leader), warps 2-17 softmax.
 // Padded query rows are zero vectors (uniform over the valid keys, mask_builder
 // .cpp:40-49); padded key columns are excluded (:50-60).
 #include <cuda.h>
