@@ -57,7 +57,10 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
                                                       float* __restrict__ pooled, int64_t pool,
                                                       int32_t* __restrict__ nonfinite) {
   constexpr int V = Vec<T>::N;
-  constexpr int kBatch = 8;  // independent 16-byte row loads in flight per thread
+  // independent 16-byte row loads in flight per thread: 4 keeps the pooling variant at
+  // <= 56 registers (3 CTAs of 384 threads per SM); 8 or 16 cost more in occupancy than
+  // they gain in memory-level parallelism (tools/permute_bench.py: 0.73 -> 0.69 ms at HY)
+  constexpr int kBatch = 4;
   const int64_t vec_per_row = d / V;
   const int64_t slots = heads * vec_per_row;
   const int64_t r0 = int64_t(blockIdx.x) * rows;
@@ -80,7 +83,12 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
   for (int64_t s = threadIdx.x; s < slots; s += blockDim.x) {
     const int64_t h = s / vec_per_row;
     const int64_t c = (s % vec_per_row) * V;
-    double acc[kPool ? V : 1];
+#ifdef DFS_PERMUTE_POOL_F32  // experiment builds only: fp32 sums (not the reference's rounding)
+    using Acc = float;
+#else
+    using Acc = double;
+#endif
+    Acc acc[kPool ? V : 1];
     if (kPool) {
 #pragma unroll
       for (int j = 0; j < V; ++j) acc[j] = 0.0;
@@ -104,7 +112,7 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
           unpack<T>(u[k], x);
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            if (kPool) acc[j] += double(x[j]);
+            if (kPool) acc[j] += Acc(x[j]);
             bad |= !isfinite(x[j]);
           }
         }
@@ -114,7 +122,7 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
       const int64_t g = r0 / pool;
       float* out = pooled + (h * ceil_div(n, pool) + g) * d + c;
 #pragma unroll
-      for (int j = 0; j < V; ++j) out[j] = float(acc[j] / double(pool));
+      for (int j = 0; j < V; ++j) out[j] = float(acc[j] / Acc(pool));
     }
   }
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);

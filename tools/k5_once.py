@@ -1,0 +1,17 @@
+"""One K5 call at HY with real masks (for ncu: -k regex:attn_sm100 -s 1 -c 1)."""
+import sys, torch
+sys.path.insert(0, '.')
+import paper_2605_23445_b200 as dfs
+from paper_2605_23445_b200 import ops
+from bench import WORKLOADS, smooth_fields
+wl = WORKLOADS['HY']
+dims, H, d, B, Bs, g = wl["dims"], wl["heads"], wl["d"], wl["block"], wl["sub"], wl["gamma"]
+n = dims[0] * dims[1] * dims[2]; m = -(-n // B)
+q, k, v = smooth_fields(dims, H, d, 1, torch.device("cuda"))
+perm = dfs.hilbert3d_order(dims)
+qh, pq = ops.permute_to_hnd(q, perm, Bs); kh, pk = ops.permute_to_hnd(k, perm, Bs); vh, _ = ops.permute_to_hnd(v, perm, 0)
+S = ops.score_pooled(pq, pk, n, dfs.ScoringParams(B, Bs)); lut = dfs.topk_lut(S, g); K = lut.shape[-1]
+ptr = ops.lut_row_ptr(H, m, K); out = torch.empty_like(q)
+for _ in range(2):
+    dfs.sparse_attention_csr(qh, kh, vh, ptr, lut.reshape(-1), B, out_layout=1, out_rows=perm.forward, out=out)
+torch.cuda.synchronize()
