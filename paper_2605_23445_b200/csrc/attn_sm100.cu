@@ -6,22 +6,23 @@
 // (top-K LUT, or every block for dense / cross attention), so masked blocks
 // cost neither bytes nor FLOPs.
 //
-// Warp roles (320 threads):
-//   warp 0      TMA producer: Q tile, then K_0, K_1, V_0, K_2, V_1, ... into a
+// Warp roles (64 + 128 * kWG threads; kWG = 4 -> 576):
+//   warp 0      TMA producer: Q tile (TMA tile::gather4 of raster rows when the
+//               reorder is fused), then K_0, K_1, K_2, V_0, K_3, V_1, ... into a
 //               ring of kStages smem slots (SWIZZLE_128B boxes of 128 x 64).
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T into a double-buffered
-//               TMEM S (QK of block j+1 overlaps the softmax of block j), then
-//               O += P_j V_j with P_j read straight from TMEM (it overwrites
-//               S_j in place, bf16) and O resident in TMEM.
-//   warps 2-9   softmax / correction / epilogue, two warpgroups that split the
-//               128 key columns of every query row (TMEM lane): each thread
-//               handles 64 logits per block, the row max is exchanged through
-//               shared memory with one named barrier per block. Online softmax
-//               in the log2 domain; O is rescaled in TMEM only when the
-//               running max grows by > 2^8 (the final normalisation uses the
-//               same stale max for O and l, so this is exact). The epilogue
-//               writes each output row straight to its raster position
-//               out_rows[i] — the unpermute (scheduler.cpp:134) is fused here.
+//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into one of three
+//               TMEM S buffers (QK runs two blocks ahead of PV, so the tensor pipe
+//               always has work queued behind each PV), then O += P_j V_j with P_j
+//               read straight from TMEM (bf16, aliasing S_j) and O resident in TMEM.
+//   warps 2..   softmax / correction / epilogue: kWG warpgroups split the 128 key
+//               columns of every query row (TMEM lane); each thread handles
+//               128 / kWG logits per block and the row max is exchanged through
+//               shared memory with one named barrier per block. Online softmax in
+//               the log2 domain, exp2 split between MUFU and an FMA-pipe polynomial;
+//               O is rescaled in TMEM only when the running max grows by > 2^8 (the
+//               final normalisation uses the same stale max for O and l, so this is
+//               exact). The epilogue writes each output row straight to its raster
+//               position out_rows[i] — the unpermute (scheduler.cpp:134) is fused here.
 // Padded keys of the last partial block get -inf logits; padded query rows
 // are computed on TMA zero-fill and never stored (attention.cpp:146-152).
 #include <cuda.h>
