@@ -141,26 +141,56 @@ __global__ void __launch_bounds__(128) topk_warp_kernel(const double* __restrict
     key[c] = i < m ? order_key(srow[i]) : 0ull;  // padding sorts below every real key (real keys have bit 63 set
                                                  // or are ~b of a negative double, never 0 for finite input)
   }
-  auto count_ge = [&](uint64_t t) {
+  // largest T with count(key >= T) >= k, built MSB-first; stop early once count == k at
+  // the probe. Two 32-bit phases instead of one 64-bit pass: the high words decide almost
+  // every row (sign, exponent and 20 mantissa bits), and a 32-bit compare is one
+  // instruction where a 64-bit one is two.
+  uint32_t hi[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) hi[c] = uint32_t(key[c] >> 32);
+  uint32_t t_hi = 0;
+  bool exact = false;
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t cand = t_hi | (1u << bit);
     int c = 0;
 #pragma unroll
-    for (int j = 0; j < CH; ++j) c += key[j] >= t;
-    return __reduce_add_sync(0xffffffffu, c);
-  };
-  // largest T with count(key >= T) >= k; stop early once count == k at the probe
-  uint64_t T = 0;
-  bool exact = false;
-  for (int bit = 63; bit >= 0; --bit) {
-    const uint64_t cand = T | (uint64_t(1) << bit);
-    const int c = count_ge(cand);
+    for (int j = 0; j < CH; ++j) c += hi[j] >= cand;
+    c = __reduce_add_sync(0xffffffffu, c);
     if (c >= k) {
-      T = cand;
+      t_hi = cand;
       if (c == k) {
         exact = true;
         break;
       }
     }
   }
+  uint32_t t_lo = 0;
+  if (!exact) {
+    // count(hi > t_hi) < k <= count(hi >= t_hi): the rest is decided among hi == t_hi
+    int gt = 0;
+    uint32_t eq = 0;  // bit j: hi[j] == t_hi
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      gt += hi[j] > t_hi;
+      eq |= uint32_t(hi[j] == t_hi) << j;
+    }
+    const int need = k - __reduce_add_sync(0xffffffffu, gt);
+    for (int bit = 31; bit >= 0; --bit) {
+      const uint32_t cand = t_lo | (1u << bit);
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) c += ((eq >> j) & 1u) && uint32_t(key[j]) >= cand;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (c >= need) {
+        t_lo = cand;
+        if (c == need) {
+          exact = true;
+          break;
+        }
+      }
+    }
+  }
+  const uint64_t T = (uint64_t(t_hi) << 32) | t_lo;
   int need_eq = k;  // keys equal to T taken, lowest indices first (stable-sort tie rule)
   if (!exact) {
     int gt = 0;
