@@ -21,6 +21,12 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// order_key on the raw bits: -0.0 maps like +0.0
+__device__ __forceinline__ uint64_t order_key_bits(uint64_t b) {
+  if ((b << 1) == 0) b = 0;
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
 __device__ __forceinline__ uint64_t order_key(double x) {
   if (x == 0.0) x = 0.0;
   const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
@@ -134,12 +140,20 @@ __global__ void __launch_bounds__(128) topk_warp_kernel(const double* __restrict
   const int64_t row = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
   if (row >= rows) return;
   const double* srow = scores + row * m;
+  // all CH loads issued before any key is formed (a per-element load -> compare chain
+  // serialised the row's L2 latency 32 times); keys from the raw bits with integer ops
   uint64_t key[CH];
+  const unsigned long long* rbits = reinterpret_cast<const unsigned long long*>(srow);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int i = c * 32 + lane;
-    key[c] = i < m ? order_key(srow[i]) : 0ull;  // padding sorts below every real key (real keys have bit 63 set
-                                                 // or are ~b of a negative double, never 0 for finite input)
+    key[c] = i < m ? __ldg(rbits + i) : 0ull;
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    // padding (0) sorts below every real key: real keys have bit 63 set or are ~b of a
+    // negative double, never 0 for finite input
+    if (c * 32 + lane < m) key[c] = order_key_bits(key[c]);
   }
   // largest T with count(key >= T) >= k, built MSB-first; stop early once count == k at
   // the probe. Two 32-bit phases instead of one 64-bit pass: the high words decide almost
