@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
   }
   __syncthreads();
   bool bad = false;
-  for (int64_t s = threadIdx.x; s < slots; s += blockDim.x) {
+  // slots split over blockIdx.y when one CTA would need more than 384 threads (keeps 3 CTAs
+  // of the pooling variant resident per SM; 40 heads x 16 chunks = 640 slots -> 2 x 320)
+  for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < slots; s += int64_t(gridDim.y) * blockDim.x) {
     const int64_t h = s / vec_per_row;
     const int64_t c = (s % vec_per_row) * V;
 #ifdef DFS_PERMUTE_POOL_F32  // experiment builds only: fp32 sums (not the reference's rounding)
@@ -174,13 +176,16 @@ int launch(const void* src, int src_layout, void* dst, int dst_layout, const uin
     // one thread per (head, 16-byte column chunk) slot when that fits a CTA: every thread
     // then walks the CTA's rows once (no second round for a remainder of slots)
     const int64_t slots = heads * (d / Vec<T>::N);
-    const int threads = slots <= 1024 ? int(ceil_div(slots, 32) * 32) : 256;
+    const int64_t ysplit = ceil_div(slots, 384);
+    const int threads = int(ceil_div(ceil_div(slots, ysplit), 32) * 32);
+    const dim3 g{unsigned(grid), unsigned(ysplit), 1u};
+    if (ysplit > 65535) return fail(DFS_E_UNSUPPORTED, "permute: rows too wide");
     if (pooled)
-      permute_kernel<T, true, kScatter><<<unsigned(grid), threads, 0, stream>>>(
-          s, src_layout, o, dst_layout, idx, n, heads, d, int(rows), pooled, pool, nonfinite);
+      permute_kernel<T, true, kScatter><<<g, threads, 0, stream>>>(s, src_layout, o, dst_layout, idx, n, heads, d,
+                                                                  int(rows), pooled, pool, nonfinite);
     else
-      permute_kernel<T, false, kScatter><<<unsigned(grid), threads, 0, stream>>>(
-          s, src_layout, o, dst_layout, idx, n, heads, d, int(rows), nullptr, 1, nonfinite);
+      permute_kernel<T, false, kScatter><<<g, threads, 0, stream>>>(s, src_layout, o, dst_layout, idx, n, heads, d,
+                                                                   int(rows), nullptr, 1, nonfinite);
   } else {
     permute_scalar_kernel<T, kScatter><<<unsigned(grid), 256, 0, stream>>>(
         s, src_layout, o, dst_layout, idx, n, heads, d, pooled, pool, nonfinite);
