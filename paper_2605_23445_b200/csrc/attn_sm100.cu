@@ -50,7 +50,7 @@ constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-constexpr uint32_t kBarMax = 1;            // named barrier ids (0 = __syncthreads)
+constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-row group (0 = __syncthreads)
 
 template <int D>
 struct Cfg {
@@ -336,6 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 2) >> 2;                    // key columns [32*wg, 32*wg + 32)
     const int r = (warp & 3) * 32 + lane;              // query row within the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
+    // A row's max / sum exchange involves only the kWG warps holding that row's slices
+    // (same warp & 3): each 32-row group synchronises on its own named barrier, so a
+    // slow warp stalls three peers instead of all sixteen softmax warps.
+    const uint32_t bar_rows = kBarRows + uint32_t(warp & 3);
     uint32_t s_iter = 0;
     float* red_max = red;                              // [parity][kWG][kBM]
     float* red_sum = red + 2 * kWG * kBM;              // [kWG][kBM]
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < kCPT; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         red_par[wg * kBM + r] = mx;
-        named_bar_sync(kBarMax, kSoftmaxThreads);      // every slice loaded S and published its max
+        named_bar_sync(bar_rows, kWG * 32);            // every slice of these rows published its max
         if (tr) trace(p, 6 + (wg & 1) * 4, s_iter);
 #pragma unroll
         for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (cnt > 0) wait_pv(s_iter - 1);
       tc_fence_after();
       red_sum[wg * kBM + r] = l;   // dedicated slots: the max slots may still be read by peers
-      named_bar_sync(kBarMax, kSoftmaxThreads);
+      named_bar_sync(bar_rows, kWG * 32);
       float l_tot = 0.f;
 #pragma unroll
       for (int w = 0; w < kWG; ++w) l_tot += red_sum[w * kBM + r];
