@@ -6,7 +6,7 @@
 // (top-K LUT, or every block for dense / cross attention), so masked blocks
 // cost neither bytes nor FLOPs.
 //
-// Warp roles (64 + 128 * kWG threads; kWG = 4 -> 576):
+// Warp roles (64 + 128 * kWG threads; kWG = 2 -> 320):
 //   warp 0      TMA producer: Q tile (TMA tile::gather4 of raster rows when the
 //               reorder is fused), then K_0, K_1, K_2, V_0, K_3, V_1, ... into a
 //               ring of kStages smem slots (SWIZZLE_128B boxes of 128 x 64).
@@ -42,14 +42,17 @@ using namespace sm100;
 constexpr int kBM = 128;         // query rows per tile (= TMEM lanes)
 constexpr int kBN = 128;         // keys per block
 #ifndef DFS_ATTN_WG
-#define DFS_ATTN_WG 4
+#define DFS_ATTN_WG 2
 #endif
 constexpr int kWG = DFS_ATTN_WG;           // softmax warpgroups splitting the 128 key columns
 constexpr int kCPT = 128 / kWG;            // key columns (logits) per softmax thread per block
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr uint32_t kTmemCols = 512;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef DFS_ATTN_RESCALE_LOG2
+#define DFS_ATTN_RESCALE_LOG2 8.0f
+#endif
+constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
 constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-row group (0 = __syncthreads)
 
 template <int D>
@@ -331,9 +334,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ============================ softmax / epilogue ============================
-    // kWG warpgroups split the 128 key columns of each block (32 per group); a thread
+    // kWG warpgroups split the 128 key columns of each block (128 / kWG each); a thread
     // owns one query row (TMEM lane) of its 32-column slice.
-    const int wg = (warp - 2) >> 2;                    // key columns [32*wg, 32*wg + 32)
+    const int wg = (warp - 2) >> 2;                    // key columns [kCPT*wg, kCPT*wg + kCPT)
     const int r = (warp & 3) * 32 + lane;              // query row within the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
     // A row's max / sum exchange involves only the kWG warps holding that row's slices
@@ -597,9 +600,9 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
 }
 
 // exp2 split between MUFU and the FMA-pipe polynomial: every POLY-th pair of a
-// thread's 32 logits goes to the polynomial (0 = all MUFU). DFS_ATTN_POLY
+// thread's logits goes to the polynomial (0 = all MUFU). DFS_ATTN_POLY
 // overrides the default for A/B measurements.
-constexpr int kDefaultPoly = 3;
+constexpr int kDefaultPoly = kWG == 2 ? 4 : 3;  // measured (tools/k5_cycles.sh): 64 / 32 logits per thread
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {

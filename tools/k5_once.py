@@ -1,10 +1,10 @@
-"""One K5 call at HY with real masks (for ncu: -k regex:attn_sm100 -s 1 -c 1)."""
+"""K5 calls at a config shape (default HY) with real masks (for ncu: -k regex:attn_sm100)."""
 import sys, torch
 sys.path.insert(0, '.')
 import paper_2605_23445_b200 as dfs
 from paper_2605_23445_b200 import ops
 from bench import WORKLOADS, smooth_fields
-wl = WORKLOADS['HY']
+wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else 'HY']
 dims, H, d, B, Bs, g = wl["dims"], wl["heads"], wl["d"], wl["block"], wl["sub"], wl["gamma"]
 n = dims[0] * dims[1] * dims[2]; m = -(-n // B)
 q, k, v = smooth_fields(dims, H, d, 1, torch.device("cuda"))
