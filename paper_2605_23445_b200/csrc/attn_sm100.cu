@@ -95,17 +95,23 @@ struct Bars {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void tile_list(const Params& p, int64_t tile, int64_t& h, int64_t& u, int32_t& beg,
-                                          int32_t& cnt) {
-  h = tile / p.mq;
-  u = tile % p.mq;
-  if (p.blk_ptr) {
-    beg = p.blk_ptr[tile];
-    cnt = p.blk_ptr[tile + 1] - beg;
-  } else {
-    beg = 0;
-    cnt = int32_t(p.mk);
+// (begin, count) of a tile's key-block list, loaded one tile ahead by every role so the
+// list pointers, the first list entry and the epilogue's output-row index are not a
+// chain of dependent global loads on each tile boundary
+struct TileMeta {
+  int32_t beg, cnt;
+};
+__device__ __forceinline__ TileMeta load_meta(const Params& p, int64_t tile) {
+  TileMeta t{0, 0};
+  if (tile < p.tiles) {
+    if (p.blk_ptr) {
+      t.beg = __ldg(p.blk_ptr + tile);
+      t.cnt = __ldg(p.blk_ptr + tile + 1) - t.beg;
+    } else {
+      t.cnt = int32_t(p.mk);
+    }
   }
+  return t;
 }
 
 #ifdef DFS_ATTN_TRACE_BUILD
@@ -215,15 +221,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       ++ring;
     };
+    TileMeta nxt = load_meta(p, blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-      int64_t h, u;
-      int32_t beg, cnt;
-      tile_list(p, tile, h, u, beg, cnt);
-      mbar_wait(&bars->q_empty, q_phase ^ 1);
-      q_phase ^= 1;
+      const int64_t h = tile / p.mq, u = tile % p.mq;
+      const int32_t beg = nxt.beg, cnt = nxt.cnt;
+      nxt = load_meta(p, tile + gridDim.x);
       {
         int rr[4] = {0, 0, 0, 0};
-        if (p.in_rows) gather_rows(h, u * kBM, rr);
+        if (p.in_rows) gather_rows(h, u * kBM, rr);  // row indices fetched while Q's slot drains
+        mbar_wait(&bars->q_empty, q_phase ^ 1);
+        q_phase ^= 1;
         issue_tile(&tm_q, h, u * kBM, sQ, &bars->q_full, rr, p.in_rows != nullptr);
       }
       // key-block list window: entries [win, win + 32) held one per lane
@@ -311,10 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       ++pv_iter;
     };
+    TileMeta nxt = load_meta(p, blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-      int64_t h, u;
-      int32_t beg, cnt;
-      tile_list(p, tile, h, u, beg, cnt);
+      const int32_t cnt = nxt.cnt;
+      nxt = load_meta(p, tile + gridDim.x);
       mbar_wait(&bars->q_full, q_phase);
       q_phase ^= 1;
       if (cnt > 0) issue_qk();
@@ -351,13 +358,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // PV_{g-3} completed (in-order tcgen05 pipe, QK_{g+1} is issued after PV_{g-2}), so the
     // barrier is never more than one phase behind the one waited for.
     auto wait_pv = [&](uint32_t g) { mbar_wait(&bars->o_done[g % C::kSBufs], (g / C::kSBufs) & 1); };
+    TileMeta nxt = load_meta(p, blockIdx.x);
+    int32_t vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-      int64_t h, u;
-      int32_t beg, cnt;
-      tile_list(p, tile, h, u, beg, cnt);
+      const int64_t h = tile / p.mq, u = tile % p.mq;
+      const int32_t beg = nxt.beg, cnt = nxt.cnt;
+      nxt = load_meta(p, tile + gridDim.x);
+      const int64_t i_row = u * kBM + r;  // this thread's query row, and its raster slot
+      const int64_t orow = i_row < p.nq && p.out_rows ? int64_t(__ldg(p.out_rows + i_row)) : i_row;
       float m = -INFINITY;
       uint64_t lsum[2] = {0, 0};  // packed fp32x2 partial row sums (2 independent chains)
-      int32_t vb_next = cnt > 0 ? block_at(p, beg, 0) : 0;
+      int32_t vb_next = vb_first;
       for (int32_t j = 0; j < cnt; ++j) {
         const int32_t vb = vb_next;
         if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);  // prefetch: keeps the LUT load off the critical path
@@ -460,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&bars->p_full[sb]);
         ++s_iter;
       }
+      vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;  // lands during the epilogue
       float l;
       {
         float a, b;
@@ -475,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float l_tot = 0.f;
 #pragma unroll
       for (int w = 0; w < kWG; ++w) l_tot += red_sum[w * kBM + r];
-      const int64_t i = u * kBM + r;
+      const int64_t i = i_row;
       // an empty key list (possible only through a caller-built CSR; the BlockMask entry
       // points refuse it like attention.cpp:133-136) yields a zero row, never stale TMEM
       const float inv_l = cnt > 0 ? 1.f / l_tot : 0.f;
@@ -495,7 +507,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kOC; ++c) ov[c] = 0u;
       }
       if (i < p.nq) {
-        const int64_t orow = p.out_rows ? int64_t(p.out_rows[i]) : i;
         __nv_bfloat16* dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
 #pragma unroll
         for (int q8 = 0; q8 < kOC / 8; ++q8) {
