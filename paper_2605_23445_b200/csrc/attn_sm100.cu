@@ -613,7 +613,7 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
 // exp2 split between MUFU and the FMA-pipe polynomial: every POLY-th pair of a
 // thread's logits goes to the polynomial (0 = all MUFU). DFS_ATTN_POLY
 // overrides the default for A/B measurements.
-constexpr int kDefaultPoly = kWG == 2 ? 4 : 3;  // measured (tools/k5_cycles.sh): 64 / 32 logits per thread
+constexpr int kDefaultPoly = 3;  // measured (tools/k5_cycles.sh) with the degree-2 polynomial
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {

@@ -360,7 +360,7 @@ __device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
 }
 
 // ex2_poly on a pair with packed fp32x2 arithmetic: clamp (2 FMNMX), round-split
-// (3 FADD2), degree-3 polynomial (3 FFMA2), exponent insertion (2 integer ops) —
+// (3 FADD2), degree-2 polynomial (2 FFMA2), exponent insertion (2 integer ops) —
 // about 5 issue slots per exponential instead of ~9 for two scalar ex2_poly calls.
 __device__ __forceinline__ uint64_t ex2_poly2(float x0, float x1) {
   x0 = fmaxf(x0, -125.f);
@@ -370,9 +370,10 @@ __device__ __forceinline__ uint64_t ex2_poly2(float x0, float x1) {
   const uint64_t t = f2_add(x, big);                          // round(x) in the low mantissa bits
   const uint64_t nf = f2_add(t, f2_pack(-12582912.f, -12582912.f));
   const uint64_t f = f2_fma(nf, f2_pack(-1.f, -1.f), x);
-  uint64_t p = f2_fma(f2_pack(0.0550405446f, 0.0550405446f), f, f2_pack(0.242285125f, 0.242285125f));
-  p = f2_fma(p, f, f2_pack(0.693254248f, 0.693254248f));
-  p = f2_fma(p, f, f2_pack(0.999950319f, 0.999950319f));
+  // degree 2 on [-0.5, 0.5]: max relative error 1.7e-3, below a bf16 half-ulp (P is
+  // rounded to bf16 for the PV MMA); -1.8 % K5 cycles against degree 3 (tools/k5_cycles.sh)
+  uint64_t p = f2_fma(f2_pack(0.23841662f, 0.23841662f), f, f2_pack(0.7034302f, 0.7034302f));
+  p = f2_fma(p, f, f2_pack(1.0004429f, 1.0004429f));
   float p0, p1, t0, t1;
   f2_unpack(p, p0, p1);
   f2_unpack(t, t0, t1);
