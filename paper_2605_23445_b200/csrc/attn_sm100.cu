@@ -80,6 +80,7 @@ struct Params {
   const uint32_t* out_rows;
   __nv_bfloat16* out;
   int out_layout;
+  int out_v8;  // output 32-byte aligned: 32-byte epilogue stores
   int in_nhd;  // 1: inputs are [N, H, d] (tensor-map coordinates (col, head, row))
   float scale_log2;
   const uint32_t* in_rows;  // fused Q reorder: logical query row i = raster token in_rows[i] (NULL: tiles)
@@ -509,13 +510,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (i < p.nq) {
         __nv_bfloat16* dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
 #pragma unroll
-        for (int q8 = 0; q8 < kOC / 8; ++q8) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(ov[8 * q8 + 0]) * inv_l, __uint_as_float(ov[8 * q8 + 1]) * inv_l);
-          w.y = pack_bf16(__uint_as_float(ov[8 * q8 + 2]) * inv_l, __uint_as_float(ov[8 * q8 + 3]) * inv_l);
-          w.z = pack_bf16(__uint_as_float(ov[8 * q8 + 4]) * inv_l, __uint_as_float(ov[8 * q8 + 5]) * inv_l);
-          w.w = pack_bf16(__uint_as_float(ov[8 * q8 + 6]) * inv_l, __uint_as_float(ov[8 * q8 + 7]) * inv_l);
-          *reinterpret_cast<uint4*>(dst + q8 * 8) = w;
+        // 32-byte stores (STG.256): half the store instructions of 16-byte ones; the store
+        // issue at the tile boundary is what holds the warps there
+        uint32_t w[kOC / 2];
+#pragma unroll
+        for (int c = 0; c < kOC / 2; ++c)
+          w[c] = pack_bf16(__uint_as_float(ov[2 * c]) * inv_l, __uint_as_float(ov[2 * c + 1]) * inv_l);
+        if (p.out_v8) {
+#pragma unroll
+          for (int q = 0; q < kOC / 16; ++q)
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + q * 16),
+                         "r"(w[8 * q + 0]), "r"(w[8 * q + 1]), "r"(w[8 * q + 2]), "r"(w[8 * q + 3]),
+                         "r"(w[8 * q + 4]), "r"(w[8 * q + 5]), "r"(w[8 * q + 6]), "r"(w[8 * q + 7])
+                         : "memory");
+        } else {  // output only 16-byte aligned
+#pragma unroll
+          for (int q = 0; q < kOC / 8; ++q)
+            *reinterpret_cast<uint4*>(dst + q * 8) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
         }
       }
     }
@@ -637,6 +648,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   p.out_rows = a.out_rows;
   p.out = static_cast<__nv_bfloat16*>(a.o);
   p.out_layout = a.out_layout;
+  p.out_v8 = (reinterpret_cast<uintptr_t>(a.o) & 31) == 0;
   p.in_nhd = a.in_layout == DFS_NHD;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.in_rows = a.in_rows;

@@ -218,3 +218,23 @@ def test_logit_jump_across_blocks(jump):
     o2 = m.sparse_attention_csr(q2, k2, v2, ptr, lut.reshape(-1), 128, layout=1, out_layout=1)
     ref2 = torch.softmax(q2.float() @ k2.float().transpose(1, 2) / d ** 0.5, -1) @ v2.float()
     assert rel(o2.float(), ref2) <= 2e-2
+
+
+def test_output_only_16_byte_aligned():
+    """The epilogue uses 32-byte stores when the output is 32-byte aligned and 16-byte
+    stores otherwise: an output view offset by 16 bytes gives the same rows."""
+    m = dfs()
+    gen = torch.Generator().manual_seed(11)
+    h, n, d = 2, 1000, 128
+    q, kk, v = (torch.randn(h, n, d, generator=gen).to(torch.bfloat16).cuda() for _ in range(3))
+    mq = -(-n // 128)
+    lut = random_lut(h, mq, mq, 3, gen).cuda()
+    ptr = m.ops.lut_row_ptr(h, mq, 3)
+    flat = torch.zeros(n * h * d + 16, dtype=torch.bfloat16, device="cuda")
+    out16 = flat[8:8 + n * h * d].view(n, h, d)
+    assert out16.data_ptr() % 32 == 16
+    o_al = m.sparse_attention_csr(q, kk, v, ptr, lut.reshape(-1), 128, out_layout=1)
+    o_16 = m.sparse_attention_csr(q, kk, v, ptr, lut.reshape(-1), 128, out_layout=1, out=out16)
+    torch.cuda.synchronize()
+    assert o_al.data_ptr() % 32 == 0
+    assert torch.equal(o_al.reshape(-1), o_16.reshape(-1))  # same NHD memory image
