@@ -103,3 +103,43 @@ def test_scorer_extreme_magnitudes():
         fast = gpu_scores(q, k, 128, 16)
         ref = ora.block_scores(q[0], k[0], 128, 16)
         assert np.abs(fast[0] - ref).max() / np.abs(ref).max() <= 1e-4, scale
+
+
+def test_fuzz_pair_scorer_vs_fp64_scorer():
+    """K3 runs as CTA pairs (two 128-row stripes of one head per pair): random head counts
+    and lengths give odd stripe counts (a padded partner stripe), grids below 148 CTAs
+    and every supported B/B_s ratio; scores must match the fp64 scorer to 1e-4."""
+    rng = np.random.default_rng(5)
+    for trial in range(8):
+        heads = int(rng.integers(1, 6))
+        n = int(rng.integers(100, 6000))
+        d = int(rng.choice([64, 128]))
+        bs = int(rng.choice([8, 16, 32, 64]))
+        q = [rng.standard_normal((n, d)).astype(np.float32) * 2 for _ in range(heads)]
+        k = [rng.standard_normal((n, d)).astype(np.float32) * 2 for _ in range(heads)]
+        fast = gpu_scores(q, k, 128, bs)
+        slow = gpu_scores(q, k, 128, bs, generic=True)
+        err = np.abs(fast - slow).max() / np.abs(slow).max()
+        assert err <= 1e-4, (trial, heads, n, d, bs, err)
+        assert np.allclose(fast.sum(-1), 128 // bs, rtol=1e-4)
+
+
+def test_topk_tie_heavy_fuzz_bit_exact():
+    """K4 (two 32-bit bisection phases) against the oracle's stable-sort selection on
+    score matrices drawn from a handful of values (massive ties, equal high words) and on
+    values that differ only in the low 32 bits of the double."""
+    m = dfs()
+    rng = np.random.default_rng(9)
+    for mm in (7, 93, 256, 929, 1500):
+        for kind in ("ties", "lowbits"):
+            if kind == "ties":
+                S = rng.choice(np.array([0.0, 1e-3, 0.25, 0.5, 1.0]), size=(mm, mm))
+            else:
+                base = np.float64(0.123456789).view(np.uint64)
+                S = (base + rng.integers(0, 1 << 20, size=(mm, mm)).astype(np.uint64)).view(np.float64)
+            for gam in (0.1, 0.37):
+                lut = m.topk_lut(torch.from_numpy(S).cuda(), gam).cpu().numpy()
+                got = np.zeros((mm, mm), bool)
+                got[np.arange(mm)[:, None], lut] = True
+                want = mask_bits_to_dense(ora.topk_select(S, gam), mm)
+                assert (got == want).all(), (mm, kind, gam)
