@@ -338,9 +338,12 @@ def run_trajectory_bench(args, wl, dfs, dev, world, rank, local, dist):
 
     kinds = {"dense": [], "update": [], "reuse": []}
     dense_flops_total = 0.0
-    for i in range(args.warmup):
+    # warm-up: one whole trajectory (>= args.warmup steps), so the update steps' kernels
+    # (pooling, scoring, top-K) and workspaces are warm too, then an empty mask cache
+    for i in range(max(args.warmup, T)):
         dfs.run_step(q, k, v, dims, params, sched, cache, layer=0, step=i % T, out=out)
     barrier()
+    cache.clear()
     steps = max(args.steps, T)
     with ClockSampler(local) as clocks:
         barrier()
