@@ -127,6 +127,19 @@ __device__ __forceinline__ int32_t block_at(const Params& p, int32_t beg, int32_
   return p.blk_ptr ? p.blk_idx[beg + j] : j;
 }
 
+// which exp2 pairs of a thread's row slice go to the FMA-pipe polynomial: POLY = n < 10
+// is every n-th pair (0 = none); POLY = 38 is pairs 1, 4, 7 of every 8
+template <int POLY>
+__device__ __forceinline__ constexpr bool use_poly(int i) {
+  if constexpr (POLY == 0) {
+    return false;
+  } else if constexpr (POLY == 38) {
+    return (0x92u >> (i % 8)) & 1u;  // pairs 1, 4, 7 of each 8
+  } else {
+    return i % POLY == POLY - 1;
+  }
+}
+
 template <int D, int POLY>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -451,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float x0, x1;
           f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
           float p0, p1;
-          if (POLY > 0 && (i % (POLY > 0 ? POLY : 1)) == POLY - 1) {
+          if (use_poly<POLY>(i)) {
             f2_unpack(ex2_poly2(x0, x1), p0, p1);
           } else {
             p0 = ex2(x0);
@@ -621,10 +634,13 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
   return DFS_OK;
 }
 
-// exp2 split between MUFU and the FMA-pipe polynomial: every POLY-th pair of a
-// thread's logits goes to the polynomial (0 = all MUFU). DFS_ATTN_POLY
+// exp2 split between MUFU and the FMA-pipe polynomial (use_poly): measured per head
+// dimension with tools/k5_cycles.sh and the degree-2 polynomial — d = 128: pairs 1, 4, 7
+// of every 8 (-1.9 % SM cycles vs every 3rd; the positions matter as much as the
+// ratio: pairs 0, 3, 6 gain only 0.5 %), d = 64: every 3rd pair. DFS_ATTN_POLY
 // overrides the default for A/B measurements.
-constexpr int kDefaultPoly = 3;  // measured (tools/k5_cycles.sh) with the degree-2 polynomial
+template <int D>
+constexpr int kDefaultPoly = D == 128 ? 38 : 3;
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
@@ -659,12 +675,12 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 16 * 256 * sizeof(unsigned long long)));
   if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 16 * 256 * sizeof(unsigned long long), stream));
 #endif
-  static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly;
+  static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly<D>;
   switch (poly) {
     case 0: rc = launch_kernel<D, 0>(mq, mk, mv, p, stream); break;
     case 2: rc = launch_kernel<D, 2>(mq, mk, mv, p, stream); break;
     case 3: rc = launch_kernel<D, 3>(mq, mk, mv, p, stream); break;
-    case 8: rc = launch_kernel<D, 8>(mq, mk, mv, p, stream); break;
+    case 38: rc = launch_kernel<D, 38>(mq, mk, mv, p, stream); break;
     default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
   }
   if (rc) return rc;
