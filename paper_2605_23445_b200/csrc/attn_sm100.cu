@@ -620,14 +620,9 @@ template <int D, int POLY>
 int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const Params& p,
                   cudaStream_t stream) {
   using C = Cfg<D>;
-  int dev = 0;
-  DFS_CUDA_CHECK(cudaGetDevice(&dev));
-  static bool attr_set[64] = {};
-  if (dev < 64 && !attr_set[dev]) {
-    DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        C::kSmem));
-    attr_set[dev] = true;
-  }
+  // per device and race-free: set on every launch (~1 us)
+  DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      C::kSmem));
   const int64_t grid = p.tiles < kNumSMs ? p.tiles : kNumSMs;
   attn_sm100_kernel<D, POLY><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
   DFS_LAUNCH_CHECK("attn_sm100");

@@ -293,13 +293,8 @@ int launch(const void* q, const void* k, int layout, const uint32_t* q_rows, int
   p.in_nhd = layout == DFS_NHD;
   p.scale_log2 = float(1.4426950408889634 / sqrt(double(D)));
   p.mass = mass;
-  int dev = 0;
-  DFS_CUDA_CHECK(cudaGetDevice(&dev));
-  static bool attr_set[64] = {};
-  if (dev < 64 && !attr_set[dev]) {
-    DFS_CUDA_CHECK(cudaFuncSetAttribute(recall_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    attr_set[dev] = true;
-  }
+  // per device and race-free: set on every launch (~1 us)
+  DFS_CUDA_CHECK(cudaFuncSetAttribute(recall_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int64_t grid = p.tiles < kNumSMs ? p.tiles : kNumSMs;
   recall_kernel<D><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, p);
   recall_reduce_kernel<<<unsigned(heads), 256, 0, stream>>>(mass, n, recall);

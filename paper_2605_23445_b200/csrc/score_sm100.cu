@@ -431,12 +431,10 @@ __global__ void factor_kernel(const unsigned* __restrict__ amax_q, const unsigne
 template <int D, int SUBS>
 int launch(const CUtensorMap* maps, const SParams& p, cudaStream_t stream) {
   using C = SCfg<D>;
-  static bool attr = false;
-  if (!attr) {
-    DFS_CUDA_CHECK(cudaFuncSetAttribute(score_sm100_kernel<D, SUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        C::kSmem));
-    attr = true;
-  }
+  // set on every launch: the attribute is per device and a one-time static flag would be
+  // wrong for a second device and racy across host threads (the call costs ~1 us)
+  DFS_CUDA_CHECK(cudaFuncSetAttribute(score_sm100_kernel<D, SUBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      C::kSmem));
   const int64_t grid = 2 * p.pitems < kNumSMs ? 2 * p.pitems : kNumSMs;  // whole pairs (kNumSMs is even)
   score_sm100_kernel<D, SUBS><<<unsigned(grid), kThreads, C::kSmem, stream>>>(maps[0], maps[1], maps[2], maps[3], p);
   DFS_LAUNCH_CHECK("score_sm100");
