@@ -392,13 +392,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 // ---- operand preparation: per-head power-of-two scale, fp16 hi/lo split ----------
 
-__global__ void absmax_kernel(const float* __restrict__ x, int64_t per_head, int heads, unsigned* __restrict__ out) {
+// pooled q (blockIdx.z = 0) and k (1) in one launch each: per-head absmax, then the
+// fp16 hi/lo split (16-byte loads); the split's first block of each head also writes
+// the logit factor fac[h] = scale_log2 / (s_q s_k)
+__global__ void absmax_kernel(const float* __restrict__ xq, const float* __restrict__ xk, int64_t per_head,
+                              int heads, unsigned* __restrict__ out) {
   const int h = blockIdx.y;
+  const float4* x = reinterpret_cast<const float4*>((blockIdx.z ? xk : xq) + h * per_head);
   float mx = 0.f;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_head; i += int64_t(gridDim.x) * blockDim.x)
-    mx = fmaxf(mx, fabsf(x[h * per_head + i]));
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_head / 4; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
   mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) atomicMax(out + h, __float_as_uint(mx));
+  if ((threadIdx.x & 31) == 0) atomicMax(out + blockIdx.z * heads + h, __float_as_uint(mx));
 }
 
 __device__ __forceinline__ float pow2_scale(unsigned bits) {
@@ -410,22 +417,34 @@ __device__ __forceinline__ float pow2_scale(unsigned bits) {
   return ldexpf(1.f, 14 - e);
 }
 
-__global__ void split_kernel(const float* __restrict__ x, int64_t per_head, const unsigned* __restrict__ amax,
-                             __half* __restrict__ hi, __half* __restrict__ lo) {
-  const int h = blockIdx.y;
-  const float s = pow2_scale(amax[h]);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_head; i += int64_t(gridDim.x) * blockDim.x) {
-    const float a = x[h * per_head + i] * s;
-    const __half hh = __float2half_rn(a);
-    hi[h * per_head + i] = hh;
-    lo[h * per_head + i] = __float2half_rn((a - __half2float(hh)) * kLoScale);
+struct SplitOut {
+  __half *hi, *lo;
+};
+__global__ void split_kernel(const float* __restrict__ xq, const float* __restrict__ xk, int64_t per_head,
+                             const unsigned* __restrict__ amax, int heads, SplitOut oq, SplitOut ok,
+                             float scale_log2, float* __restrict__ fac) {
+  const int h = blockIdx.y, z = blockIdx.z;
+  if (blockIdx.x == 0 && z == 0 && threadIdx.x == 0)
+    fac[h] = scale_log2 / (pow2_scale(amax[h]) * pow2_scale(amax[heads + h]));
+  const float s = pow2_scale(amax[z * heads + h]);
+  const float4* x = reinterpret_cast<const float4*>((z ? xk : xq) + h * per_head);
+  const SplitOut o = z ? ok : oq;
+  __half2* hi = reinterpret_cast<__half2*>(o.hi + h * per_head);
+  __half2* lo = reinterpret_cast<__half2*>(o.lo + h * per_head);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < per_head / 4; i += int64_t(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    const float a[4] = {v.x * s, v.y * s, v.z * s, v.w * s};
+    __half hh[4], ll[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      hh[j] = __float2half_rn(a[j]);
+      ll[j] = __float2half_rn((a[j] - __half2float(hh[j])) * kLoScale);
+    }
+    hi[2 * i] = __halves2half2(hh[0], hh[1]);
+    hi[2 * i + 1] = __halves2half2(hh[2], hh[3]);
+    lo[2 * i] = __halves2half2(ll[0], ll[1]);
+    lo[2 * i + 1] = __halves2half2(ll[2], ll[3]);
   }
-}
-
-__global__ void factor_kernel(const unsigned* __restrict__ amax_q, const unsigned* __restrict__ amax_k, int heads,
-                              float scale_log2, float* __restrict__ fac) {
-  const int h = threadIdx.x + blockIdx.x * blockDim.x;
-  if (h < heads) fac[h] = scale_log2 / (pow2_scale(amax_q[h]) * pow2_scale(amax_k[h]));
 }
 
 template <int D, int SUBS>
@@ -477,13 +496,11 @@ int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t 
   float* tmax = tsum + int64_t(kNumSMs) * m_blocks * kRows;
   (void)nkt_keys;
   DFS_CUDA_CHECK(cudaMemsetAsync(amax, 0, sizeof(unsigned) * size_t(2 * heads), stream));
-  dim3 g(unsigned(ceil_div(per_head, 256) < 64 ? ceil_div(per_head, 256) : 64), unsigned(heads));
-  absmax_kernel<<<g, 256, 0, stream>>>(pq, per_head, int(heads), amax);
-  absmax_kernel<<<g, 256, 0, stream>>>(pk, per_head, int(heads), amax + heads);
-  split_kernel<<<g, 256, 0, stream>>>(pq, per_head, amax, qh, ql);
-  split_kernel<<<g, 256, 0, stream>>>(pk, per_head, amax + heads, kh, kl);
+  dim3 g(unsigned(ceil_div(per_head / 4, 256) < 64 ? ceil_div(per_head / 4, 256) : 64), unsigned(heads), 2u);
+  absmax_kernel<<<g, 256, 0, stream>>>(pq, pk, per_head, int(heads), amax);
   const float scale_log2 = float(1.4426950408889634 / sqrt(double(d)));
-  factor_kernel<<<1, 256, 0, stream>>>(amax, amax + heads, int(heads), scale_log2, fac);
+  split_kernel<<<g, 256, 0, stream>>>(pq, pk, per_head, amax, int(heads), SplitOut{qh, ql}, SplitOut{kh, kl},
+                                      scale_log2, fac);
   DFS_LAUNCH_CHECK("score_sm100 prep");
 
   CUtensorMap maps[4];
