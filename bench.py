@@ -609,10 +609,11 @@ def main():
             cpu = cpu_baseline(wl)
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "sample": f"failed: {ex}"}
-    # our kernels per update-step call (dfs_run_step): q pooling (read-only, gathered), k permute+pool,
-    # v permute, scorer prep (2 absmax, 2 fp16 split, 1 factor) + 1 tcgen05 scorer, 1 top-K, 1 LUT row
-    # pointers, 1 attention (TMA-gathered Q reorder + fused unpermute)
-    launches_per_step = 3 + 6 + 1 + 1 + 1
+    # our kernels per update-step call (dfs_run_step; tools/step_timeline.py lists them): q pooling
+    # (read-only, gathered), k permute+pool, v permute, scorer prep (q+k absmax, q+k fp16 split with
+    # the logit factor) + 1 tcgen05 scorer, 1 top-K, 1 LUT row pointers, 1 attention (TMA-gathered Q
+    # reorder + fused unpermute)
+    launches_per_step = 3 + 3 + 1 + 1 + 1
     res = {
         "metric": metric_for(args.workload), "value": dense_flops / (ms_max * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
