@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 2) >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
+    const uint32_t bar_rows = 2 + uint32_t(warp & 3);  // named barriers 2..5, one per 32-row group
     float* red_max = red;                    // [parity][kWG][kBM]
     float* red_za = red + 2 * kWG * kBM;     // [kWG][kBM]
     float* red_zm = red + 3 * kWG * kBM;     // [kWG][kBM]
@@ -203,34 +205,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->s_free[sb]);  // S_g is in registers: the buffer may be reused
+        // every block but the partial last one is full: the per-element bounds test stays
+        // out of the hot loop (as a runtime test it is if-converted into selects)
+        auto block = [&](auto mask_tag, int valid) {
+          constexpr bool kMask = decltype(mask_tag)::value;
+          float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (!kMask || i < valid) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
+          float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+          float* red_par = red_max + (g & 1) * kWG * kBM;
+          red_par[wg * kBM + r] = mx;
+          named_bar_sync(bar_rows, kWG * 32);  // only the warps holding these rows' slices
+#pragma unroll
+          for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
+          const float m_new = fmaxf(m, mx * p.scale_log2);
+          if (m_new > m) {
+            const float a = ex2(m - m_new);
+            za *= a;
+            zm *= a;
+            m = m_new;
+          }
+          // exp2 in packed fp32x2; pairs 1, 4, 7 of every 8 on the FMA-pipe polynomial
+          const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
+          uint64_t e2 = 0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x0, x1;
+            f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
+            float p0, p1;
+            if ((0x92u >> (i % 8)) & 1u) {
+              f2_unpack(ex2_poly2(x0, x1), p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            if (kMask) {
+              if (2 * i >= valid) p0 = 0.f;
+              if (2 * i + 1 >= valid) p1 = 0.f;
+            }
+            e2 = f2_add(e2, f2_pack(p0, p1));
+          }
+          float e0, e1;
+          f2_unpack(e2, e0, e1);
+          return e0 + e1;
+        };
         const int valid = int(min(int64_t(kBN), p.n - v * kBN)) - wg * 32;
-        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i < valid) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
-        float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-        float* red_par = red_max + (g & 1) * kWG * kBM;
-        red_par[wg * kBM + r] = mx;
-        named_bar_sync(kBarMax, kSoftmaxThreads);
-#pragma unroll
-        for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
-        const float m_new = fmaxf(m, mx * p.scale_log2);
-        if (m_new > m) {
-          const float a = ex2(m - m_new);
-          za *= a;
-          zm *= a;
-          m = m_new;
-        }
-        float e0 = 0.f, e1 = 0.f;
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float x0 = i < valid ? ex2(fmaf(__uint_as_float(sv[i]), p.scale_log2, -m)) : 0.f;
-          const float x1 = i + 1 < valid ? ex2(fmaf(__uint_as_float(sv[i + 1]), p.scale_log2, -m)) : 0.f;
-          e0 += x0;
-          e1 += x1;
-        }
-        za += e0 + e1;
-        if (sel) zm += e0 + e1;
+        const float e = valid >= 32 ? block(std::false_type{}, 32) : block(std::true_type{}, valid);
+        za += e;
+        if (sel) zm += e;
       }
       red_za[wg * kBM + r] = za;
       red_zm[wg * kBM + r] = zm;
