@@ -11,9 +11,9 @@
 // N x N storage. One launch per call; a second tiny kernel reduces the per-row
 // masses to a per-head recall in fp64.
 //
-// Warp roles (576 threads): 0 TMA producer (Q, then every K block in order),
+// Warp roles (64 + 128 * kWG threads): 0 TMA producer (Q, then every K block in order),
 // 1 MMA issuer (S_j into one of three TMEM buffers; S_{j+3} waits until the
-// softmax has read S_j), 2-17 four warpgroups splitting each block's 128 key
+// softmax has read S_j), 2.. kWG warpgroups splitting each block's 128 key
 // columns. Padded keys (partial last block) are excluded, padded query rows are
 // not counted.
 #include <cuda.h>
@@ -34,7 +34,11 @@ namespace {
 using namespace sm100;
 
 constexpr int kBM = 128, kBN = 128;
-constexpr int kWG = 4;
+#ifndef DFS_RECALL_WG
+#define DFS_RECALL_WG 2
+#endif
+constexpr int kWG = DFS_RECALL_WG;      // softmax warpgroups splitting each block's 128 key columns
+constexpr int kCPT = 128 / kWG;        // key columns per softmax thread
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr uint32_t kBarMax = 1;
@@ -199,8 +203,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sb = g % 3;
         mbar_wait(&bars->s_full[sb], (g / 3) & 1);
         tc_fence_after();
-        uint32_t sv[32];
-        tmem_ld32(tmem + lane_addr + sb * 128 + wg * 32, sv);
+        uint32_t sv[kCPT];
+#pragma unroll
+        for (int c = 0; c < kCPT / 32; ++c)
+          tmem_ld32(tmem + lane_addr + sb * 128 + wg * kCPT + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * c));
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -211,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           constexpr bool kMask = decltype(mask_tag)::value;
           float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
+          for (int i = 0; i < kCPT; ++i)
             if (!kMask || i < valid) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
           float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
           float* red_par = red_max + (g & 1) * kWG * kBM;
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
           uint64_t e2 = 0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < kCPT / 2; ++i) {
             float x0, x1;
             f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
             float p0, p1;
@@ -250,8 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           f2_unpack(e2, e0, e1);
           return e0 + e1;
         };
-        const int valid = int(min(int64_t(kBN), p.n - v * kBN)) - wg * 32;
-        const float e = valid >= 32 ? block(std::false_type{}, 32) : block(std::true_type{}, valid);
+        const int valid = int(min(int64_t(kBN), p.n - v * kBN)) - wg * kCPT;
+        const float e = valid >= kCPT ? block(std::false_type{}, kCPT) : block(std::true_type{}, valid);
         za += e;
         if (sel) zm += e;
       }
