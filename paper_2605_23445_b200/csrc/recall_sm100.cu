@@ -184,7 +184,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = (warp - 2) >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
-    const uint32_t bar_rows = 2 + uint32_t(warp & 3);  // named barriers 2..5, one per 32-row group
     float* red_max = red;                    // [parity][kWG][kBM]
     float* red_za = red + 2 * kWG * kBM;     // [kWG][kBM]
     float* red_zm = red + 3 * kWG * kBM;     // [kWG][kBM]
@@ -219,12 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < kCPT; ++i)
             if (!kMask || i < valid) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
-          float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-          float* red_par = red_max + (g & 1) * kWG * kBM;
-          red_par[wg * kBM + r] = mx;
-          named_bar_sync(bar_rows, kWG * 32);  // only the warps holding these rows' slices
-#pragma unroll
-          for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
+          // each slice keeps its own running max (no P is shared between slices here, unlike
+          // K5): no per-block exchange; the slices' (max, sums) merge once per tile
+          const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
           const float m_new = fmaxf(m, mx * p.scale_log2);
           if (m_new > m) {
             const float a = ex2(m - m_new);
@@ -261,15 +257,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         za += e;
         if (sel) zm += e;
       }
+      red_max[wg * kBM + r] = m;
       red_za[wg * kBM + r] = za;
       red_zm[wg * kBM + r] = zm;
       named_bar_sync(kBarMax, kSoftmaxThreads);
       if (wg == 0) {
+        float mm = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kWG; ++w) mm = fmaxf(mm, red_max[w * kBM + r]);
         float ta = 0.f, tm = 0.f;
 #pragma unroll
         for (int w = 0; w < kWG; ++w) {
-          ta += red_za[w * kBM + r];
-          tm += red_zm[w * kBM + r];
+          const float mw = red_max[w * kBM + r];
+          const float sc = mw > -INFINITY ? ex2(mw - mm) : 0.f;
+          ta += red_za[w * kBM + r] * sc;
+          tm += red_zm[w * kBM + r] * sc;
         }
         const int64_t i = u * kBM + r;
         if (i < p.n) p.mass[h * p.n + i] = tm / ta;
