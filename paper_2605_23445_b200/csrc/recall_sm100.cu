@@ -12,7 +12,7 @@
 // masses to a per-head recall in fp64.
 //
 // Warp roles (64 + 128 * kWG threads): 0 TMA producer (Q, then every K block in order),
-// 1 MMA issuer (S_j into one of three TMEM buffers; S_{j+3} waits until the
+// 1 MMA issuer (S_j into one of kSBufs TMEM buffers; S_{j+kSBufs} waits until the
 // softmax has read S_j), 2.. kWG warpgroups splitting each block's 128 key
 // columns. Padded keys (partial last block) are excluded, padded query rows are
 // not counted.
@@ -39,6 +39,10 @@ constexpr int kBM = 128, kBN = 128;
 #endif
 constexpr int kWG = DFS_RECALL_WG;      // softmax warpgroups splitting each block's 128 key columns
 constexpr int kCPT = 128 / kWG;        // key columns per softmax thread
+#ifndef DFS_RECALL_SBUFS
+#define DFS_RECALL_SBUFS 4
+#endif
+constexpr int kSBufs = DFS_RECALL_SBUFS;  // TMEM S buffers (no O here: all 512 columns can hold S)
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr uint32_t kBarMax = 1;
@@ -69,7 +73,7 @@ struct RParams {
 
 struct RBars {
   uint64_t q_full, q_empty;
-  uint64_t s_full[3], s_free[3];
+  uint64_t s_full[4], s_free[4];
   uint64_t k_full[12], k_empty[12];
   uint32_t tmem_base;
 };
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bars->q_full, 1);
     mbar_init(&bars->q_empty, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < kSBufs; ++i) {
       mbar_init(&bars->s_full[i], 1);
       mbar_init(&bars->s_free[i], kSoftmaxThreads / 32);
     }
@@ -159,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars->q_full, q_phase);
       q_phase ^= 1;
       for (int64_t v = 0; v < mk; ++v, ++g) {
-        const uint32_t sb = g % 3;
-        if (g >= 3) mbar_wait(&bars->s_free[sb], ((g / 3) - 1) & 1);  // softmax read S_{g-3}
+        const uint32_t sb = g % kSBufs;
+        if (g >= kSBufs) mbar_wait(&bars->s_free[sb], ((g / kSBufs) - 1) & 1);  // softmax read S_{g-kSBufs}
         const uint32_t slot = ring % C::kStages;
         mbar_wait(&bars->k_full[slot], (ring / C::kStages) & 1);
         ++ring;
@@ -199,8 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++cur;
           next_sel = cur < cnt ? p.blk_idx[beg + cur] : -1;
         }
-        const uint32_t sb = g % 3;
-        mbar_wait(&bars->s_full[sb], (g / 3) & 1);
+        const uint32_t sb = g % kSBufs;
+        mbar_wait(&bars->s_full[sb], (g / kSBufs) & 1);
         tc_fence_after();
         uint32_t sv[kCPT];
 #pragma unroll
