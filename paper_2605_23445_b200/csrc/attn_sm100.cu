@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st16(o_addr, ov);
           }
         }
-        // p = 2^(s*scale - m); every POLY-th pair on the FMA pipe (offloads MUFU)
+        // p = 2^(s*scale - m); the use_poly<POLY> pairs on the FMA pipe (offloads MUFU)
         const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
         uint32_t pk[kCPT / 2];
 #pragma unroll
