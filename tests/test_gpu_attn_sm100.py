@@ -238,3 +238,20 @@ def test_output_only_16_byte_aligned():
     torch.cuda.synchronize()
     assert o_al.data_ptr() % 32 == 0
     assert torch.equal(o_al.reshape(-1), o_16.reshape(-1))  # same NHD memory image
+
+
+@pytest.mark.parametrize("nk", [77, 226, 512])
+def test_text_cross_attention_shapes(nk):
+    """Video queries attending to a short text sequence (Nk < one or a few key blocks,
+    partial last block) through K5 with a full list, against a torch fp32 reference."""
+    m = dfs()
+    gen = torch.Generator().manual_seed(nk)
+    h, nq, d = 3, 4096 + 64, 128
+    q = torch.randn(nq, h, d, generator=gen).to(torch.bfloat16).cuda()
+    k = torch.randn(nk, h, d, generator=gen).to(torch.bfloat16).cuda()
+    v = torch.randn(nk, h, d, generator=gen).to(torch.bfloat16).cuda()
+    o = m.full_attention_output(q, k, v)
+    torch.cuda.synchronize()
+    qf, kf, vf = (x.float().transpose(0, 1) for x in (q, k, v))
+    ref = (torch.softmax(qf @ kf.transpose(1, 2) / d ** 0.5, -1) @ vf).transpose(0, 1)
+    assert rel(o.float(), ref) <= 2e-2
