@@ -37,7 +37,12 @@
 extern "C" {
 #endif
 
-#define DFS_ABI_VERSION 1
+#define DFS_ABI_VERSION 2
+
+/* attention.hpp:16 kMaxDenseScoreRows: up to this many tokens a DFS_F32 step runs the
+ * compatibility kernels (fp64 softmax arithmetic, the reference's 1e-5 tolerances);
+ * past it, fp32 inputs are rounded to bf16 for the tcgen05 kernels (2e-2 tolerance). */
+#define DFS_COMPAT_MAX_ROWS 4096
 
 enum dfs_status {
   DFS_OK = 0,
@@ -87,6 +92,11 @@ int dfs_validate_permutation(dfs_handle* h, const uint32_t* fwd, int64_t n, int*
 int dfs_permute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype,
                      const uint32_t* idx, int64_t n, int64_t heads, int64_t d, float* pooled,
                      int64_t pool, int32_t* nonfinite, dfs_stream stream);
+/* Element type conversion of `count` elements (DFS_F32 <-> DFS_BF16, round to
+ * nearest even); ORs 1 into *nonfinite (optional, device) when a source element
+ * is NaN/Inf. Used to feed fp32 Matrix inputs to the bf16 tensor-core kernels. */
+int dfs_cast(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t count, int32_t* nonfinite,
+             dfs_stream stream);
 /* Inverse direction: dst row idx[i] <- src row i (scatter), i.e.
  * apply_permutation(invert_permutation(p), x) without materialising inv. */
 int dfs_unpermute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype,
@@ -182,6 +192,9 @@ int dfs_mask_cache_get(dfs_handle* h, int layer, int head, uint8_t* bits, int* l
 int dfs_mask_cache_store(dfs_handle* h, int layer, int head, const uint8_t* bits, int64_t m,
                          int64_t block, int step, dfs_stream stream);
 int dfs_mask_cache_size(dfs_handle* h, int64_t* n);
+/* Geometry of the cached (layer, head) mask: block count m, block size and last
+ * update step (any pointer may be NULL). DFS_E_INVALID when absent. */
+int dfs_mask_cache_info(dfs_handle* h, int layer, int head, int64_t* m, int64_t* block, int* last_update_step);
 
 /* scheduler.cpp:91-135 run_step for ALL heads of one layer at once.
  * q, k, v, o: [N, H, d] bf16 raster-order activations (the DiT layout).
@@ -204,7 +217,12 @@ typedef struct {
   int layer;
   int step;
   int force_dense;
-  int32_t* nonfinite;    /* optional device flag */
+  /* Non-finite input is an error (attention.cpp:19-20): the step ORs a device flag
+   * in the passes that read q/k/v anyway (K2, or a check pass on dense / reuse
+   * steps), reads it back once before it scores or touches the mask cache, and
+   * returns DFS_E_INVALID with the cache and output untouched. `nonfinite`
+   * optionally names the device flag to use (caller-zeroed); NULL = the handle's. */
+  int32_t* nonfinite;
   /* outputs (host, optional) */
   int* dense_out;        /* 1 if the step ran dense */
   double* budget_out;    /* budget (1.0 when dense) */
@@ -214,6 +232,13 @@ typedef struct {
    * (scheduler.cpp:129-131 record_recall), streamed without the N x N matrix, so
    * it is available past the reference's 4096-row cap (dfs_block_recall). */
   double* recall_out;
+  /* ABI 2. dtype of q/k/v/o: DFS_BF16 (0, the performance path) or DFS_F32 (the
+   * drop-in Matrix path: n <= DFS_COMPAT_MAX_ROWS runs fp64-arithmetic compatibility
+   * kernels bit-identical to dfs::build_mask / block_sparse_attention; larger n pools
+   * and scores from the fp32 values (fp32-accurate tcgen05 scorer) and attends in bf16
+   * through K5, output converted back to fp32). */
+  int dtype;
+  int64_t dv; /* head dim of v / o; 0 = d (dv != d: DFS_F32 with n <= DFS_COMPAT_MAX_ROWS only) */
 } dfs_step_args;
 int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
 

@@ -3,7 +3,7 @@
  * Independent C11 restatement of the reference hot path; see dfs_oracle.h.
  * fp64 accumulation and fp32 storage exactly where the reference has them, so
  * that on the same host (same libm) the outputs are bit-identical to the
- * reference library — verified by tests/test_oracle_vs_ref.py. Loops over
+ * reference library — verified by tests/test_oracle.py. Loops over
  * independent rows / query blocks are OpenMP-parallel; every reduction whose
  * order the reference fixes stays sequential inside one thread, so results do
  * not depend on the thread count.

@@ -53,7 +53,7 @@ class StepArgs(C.Structure):
                 ("sub_block", _i64), ("layer", _i32), ("step", _i32), ("force_dense", _i32),
                 ("nonfinite", _p), ("dense_out", C.POINTER(_i32)), ("budget_out", C.POINTER(_dbl)),
                 ("updated_out", C.POINTER(_i32)), ("sparsity_out", C.POINTER(_dbl)),
-                ("recall_out", C.POINTER(_dbl))]
+                ("recall_out", C.POINTER(_dbl)), ("dtype", _i32), ("dv", _i64)]
 
 
 _SIGS = {
@@ -82,6 +82,8 @@ _SIGS = {
     "dfs_mask_cache_get": (_i32, [_p, _i32, _i32, _p, C.POINTER(_i32), C.POINTER(_i64), _p]),
     "dfs_mask_cache_store": (_i32, [_p, _i32, _i32, _p, _i64, _i64, _i32, _p]),
     "dfs_mask_cache_size": (_i32, [_p, C.POINTER(_i64)]),
+    "dfs_mask_cache_info": (_i32, [_p, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32)]),
+    "dfs_cast": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
     "dfs_run_step": (_i32, [_p, C.POINTER(Schedule), C.POINTER(StepArgs), _p]),
     "dfs_softmax_scores": (_i32, [_p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _dbl, _p, _p]),
     "dfs_aggregate_scores": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p]),

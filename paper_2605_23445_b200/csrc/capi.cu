@@ -33,6 +33,8 @@ int permute_rows_impl(const void* src, int src_layout, void* dst, int dst_layout
                       const uint32_t* idx, int64_t n, int64_t heads, int64_t d, float* pooled,
                       int64_t pool, int32_t* nonfinite, bool scatter, cudaStream_t stream);
 int finite_check_impl(const void* x, int64_t count, int dtype, int32_t* flag, cudaStream_t stream);
+int cast_impl(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t count, int32_t* nonfinite,
+              cudaStream_t stream);
 int score_blocks_generic(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
                          int64_t sub_block, double* S, float* P_ws, int64_t P_ws_floats, cudaStream_t stream);
 int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
@@ -142,10 +144,14 @@ struct dfs_handle {
   Buf scratch_i32, flag;
   Buf k_hnd, v_hnd, pooled_q, pooled_k, scores, score_ws, lut, sel, counts;
   Buf tmp_ptr, tmp_idx, recall_ws;
+  Buf step_flag;                         // the step's non-finite flag (dfs_step_args.nonfinite == NULL)
+  Buf q16, k16, v16, o16;                // DFS_F32 steps past the compatibility cap: bf16 copies
+  Buf f32_q, f32_k, f32_v, probs, bits;  // DFS_F32 compatibility steps: reordered fp32 [H, N, d]
   int64_t total_bytes() const {
     int64_t t = 0;
     for (const Buf* b : {&scratch_i32, &flag, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
-                         &lut, &sel, &counts, &tmp_ptr, &tmp_idx, &recall_ws})
+                         &lut, &sel, &counts, &tmp_ptr, &tmp_idx, &recall_ws, &step_flag, &q16, &k16, &v16,
+                         &o16, &f32_q, &f32_k, &f32_v, &probs, &bits})
       t += int64_t(b->bytes);
     return t;
   }
@@ -654,37 +660,180 @@ int dfs_block_recall(dfs_handle* h, const void* q, const void* k, int layout, co
   return DFS_OK;
 }
 
+// ------------------------------------------------------------- misc --------
+int dfs_cast(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t count, int32_t* nonfinite,
+             dfs_stream stream) {
+  if (!src || !dst) return fail(DFS_E_INVALID, "cast: null pointer");
+  return cast_impl(src, src_dtype, dst, dst_dtype, count, nonfinite, as_stream(stream));
+}
+
+int dfs_mask_cache_info(dfs_handle* h, int layer, int head, int64_t* m, int64_t* block, int* last_update_step) {
+  if (!h) return fail(DFS_E_INVALID, "null handle");
+  auto it = h->masks.find(layer);
+  if (it == h->masks.end() || head < 0 || head >= int(it->second.head.size()) ||
+      !it->second.head[size_t(head)].valid)
+    return fail(DFS_E_INVALID, "mask_cache_info: no entry for (layer, head)");
+  if (m) *m = it->second.m;
+  if (block) *block = it->second.block;
+  if (last_update_step) *last_update_step = it->second.head[size_t(head)].last_update_step;
+  return DFS_OK;
+}
+
+}  // extern "C"
+
+namespace capi_detail {
+
+// Reads the step's non-finite flag back (one stream sync, before anything is scored or
+// cached): the reference throws from check_qkv / attention_scores before build_mask
+// stores a mask (attention.cpp:19-20, scheduler.cpp:114-116), so a NaN step leaves the
+// cache and the output untouched here too.
+int check_flag(const int32_t* flag, cudaStream_t s) {
+  int32_t bad = 0;
+  DFS_CUDA_CHECK(cudaMemcpyAsync(&bad, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  DFS_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (bad) return fail(DFS_E_INVALID, "attention: non-finite input");
+  return DFS_OK;
+}
+
+// attention_recall(attention_scores(rq, rk), mask) per head on the fp32 compatibility
+// path (scheduler.cpp:129-131 at n <= kMaxDenseScoreRows): fp64 logits, fp32
+// probabilities, the reference's recall sums (dropin.cu), the head's mask taken from the
+// layer's device CSR.
+int compat_recall(dfs_handle* h, const LayerMasks& L, const float* rq, const float* rk, int64_t H, int64_t n,
+                  int64_t d, double* recall_out, cudaStream_t s) {
+  int rc;
+  const int64_t m = L.m;
+  if ((rc = h->probs.ensure(sizeof(float) * size_t(n * n))) || (rc = h->sel.ensure(size_t(m * m))) ||
+      (rc = h->bits.ensure(size_t((m * m + 7) / 8))))
+    return rc;
+  for (int64_t hh = 0; hh < H; ++hh) {
+    if ((rc = dfs_softmax_scores(rq + hh * n * d, rk + hh * n * d, 1, n, n, n, n, d, 0.0, h->probs.as<float>(), s)))
+      return rc;
+    DFS_CUDA_CHECK(cudaMemsetAsync(h->sel.p, 0, size_t(m * m), s));
+    csr_to_bits_kernel<<<unsigned(m), 64, 0, s>>>(L.ptr.as<int32_t>(), L.idx.as<int32_t>(), m, hh * m,
+                                                  h->sel.as<uint8_t>());
+    pack_sel_kernel<<<unsigned(ceil_div((m * m + 7) / 8, 256)), 256, 0, s>>>(h->sel.as<uint8_t>(), m * m,
+                                                                           h->bits.as<uint8_t>());
+    DFS_LAUNCH_CHECK("compat_recall");
+    if ((rc = dfs_attention_recall(h->probs.as<float>(), n, n, h->bits.as<uint8_t>(), m, L.block,
+                                   recall_out + hh, s)))
+      return rc;
+  }
+  return DFS_OK;
+}
+
+// the compatibility scorer, batched over heads: subblock_scores (fp64 logits, fp32
+// probabilities, padded rows uniform; mask_builder.cpp:30-62, attention.cpp:105-123) then
+// aggregate_scores (fp64 tile sums, mask_builder.cpp:64-80) — the kernels behind
+// dfs::block_scores at n <= kMaxDenseScoreRows
+int compat_scores(dfs_handle* h, const float* pq, const float* pk, int64_t H, int64_t n, int64_t d, int64_t B,
+                  int64_t Bs, double* S, cudaStream_t s) {
+  const int64_t subs = B / Bs, m = ceil_div(n, B), valid = ceil_div(n, Bs), rows = m * subs;
+  int64_t batch = (int64_t(1) << 26) / (rows * rows);  // <= 256 MB of probabilities per launch
+  batch = batch < 1 ? 1 : (batch > H ? H : batch);
+  int rc;
+  if ((rc = h->probs.ensure(sizeof(float) * size_t(batch * rows * rows)))) return rc;
+  for (int64_t h0 = 0; h0 < H; h0 += batch) {
+    const int64_t hb = H - h0 < batch ? H - h0 : batch;
+    if ((rc = dfs_softmax_scores(pq + h0 * valid * d, pk + h0 * valid * d, hb, valid, rows, valid, rows, d, 0.0,
+                                 h->probs.as<float>(), s)) ||
+        (rc = dfs_aggregate_scores(h->probs.as<float>(), hb, m, m, subs, S + h0 * m * m, s)))
+      return rc;
+  }
+  return DFS_OK;
+}
+
+int attn_simple(dfs_handle* h, const void* q, const void* k, const void* v, void* o, int dtype, int in_layout,
+                const uint32_t* in_rows, int out_layout, const uint32_t* out_rows, int64_t H, int64_t n, int64_t d,
+                int64_t dv, int64_t B, const int32_t* blk_ptr, const int32_t* blk_idx, cudaStream_t s) {
+  dfs_attn_args at{};
+  at.q = q;
+  at.k = k;
+  at.v = v;
+  at.o = o;
+  at.dtype = dtype;
+  at.in_layout = in_layout;
+  at.in_rows = in_rows;
+  at.out_layout = out_layout;
+  at.out_rows = out_rows;
+  at.heads = H;
+  at.nq = n;
+  at.nk = n;
+  at.d = d;
+  at.dv = dv == d ? 0 : dv;
+  at.block = B;
+  at.blk_ptr = blk_ptr;
+  at.blk_idx = blk_idx;
+  return attn_dispatch(h, at, s);
+}
+
+}  // namespace capi_detail
+using namespace capi_detail;
+
+extern "C" {
+
 // ------------------------------------------------------------ run_step -----
+// scheduler.cpp:91-135 run_step for all heads of a layer. Three input regimes:
+//   bf16            the performance path: K2 (pool / permute), K3 tcgen05, K4, K5 tcgen05
+//                   with the Q gather and the unpermute fused in;
+//   fp32, n <= cap  compatibility kernels (fp64 softmax arithmetic) bit-identical to the
+//                   dfs:: Matrix operators the reference's unit suites pin at 1e-5;
+//   fp32, n > cap   pooling and scoring from the fp32 values (tcgen05 fp16x3 = fp32
+//                   accurate), inputs rounded to bf16 for K5, output converted back.
 int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* a, dfs_stream stream) {
   if (int rc = check_handle(h)) return rc;
   if (!a || !a->q || !a->k || !a->v || !a->o) return fail(DFS_E_INVALID, "run_step: null pointer");
   cudaStream_t s = as_stream(stream);
   const int64_t n = a->n, H = a->heads, d = a->d, B = a->block, Bs = a->sub_block;
+  const int64_t dv = a->dv > 0 ? a->dv : d;
+  const int dtype = a->dtype;
+  if (dtype != DFS_BF16 && dtype != DFS_F32) return fail(DFS_E_INVALID, "run_step: dtype must be bf16 or f32");
   if (n < 1 || H < 1 || d < 1) return fail(DFS_E_INVALID, "attention: empty input");
   if (Bs < 1 || B < Bs) return fail(DFS_E_INVALID, "ScoringParams: need 1 <= sub_block_size <= block_size");
   if (B % Bs) return fail(DFS_E_INVALID, "ScoringParams: sub_block_size must divide block_size");
+  const bool compat = dtype == DFS_F32 && n <= DFS_COMPAT_MAX_ROWS;
+  if (dv != d && !compat)
+    return fail(DFS_E_UNSUPPORTED, "run_step: dv != d only on the fp32 compatibility path (n <= 4096)");
   double budget;
   if (int rc = dfs_schedule_budget_at(sched, a->step, &budget)) return rc;
   const int64_t m = ceil_div(n, B);
+  int rc;
+  int32_t* flag = a->nonfinite;
+  if (!flag) {
+    if ((rc = h->step_flag.ensure(sizeof(int32_t)))) return rc;
+    flag = h->step_flag.as<int32_t>();
+    DFS_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+  }
+  const size_t tok16 = sizeof(__nv_bfloat16) * size_t(n * H * d);
+  // fp32 inputs past the cap: bf16 copies for the tensor-core kernels (finite check folded in)
+  auto cast_inputs = [&]() -> int {
+    int r;
+    if ((r = h->q16.ensure(tok16)) || (r = h->k16.ensure(tok16)) || (r = h->v16.ensure(tok16))) return r;
+    if ((r = cast_impl(a->q, DFS_F32, h->q16.p, DFS_BF16, n * H * d, flag, s)) ||
+        (r = cast_impl(a->k, DFS_F32, h->k16.p, DFS_BF16, n * H * d, flag, s)) ||
+        (r = cast_impl(a->v, DFS_F32, h->v16.p, DFS_BF16, n * H * d, flag, s)))
+      return r;
+    return DFS_OK;
+  };
 
   if (budget < 0.0 || a->force_dense) {  // scheduler.cpp:99-105: dense, raster order, no reorder
-    if (a->nonfinite)
-      for (const void* x : {a->q, a->k, a->v})
-        if (int rc = finite_check_impl(x, n * H * d, DFS_BF16, a->nonfinite, s)) return rc;
-    dfs_attn_args at{};
-    at.q = a->q;
-    at.k = a->k;
-    at.v = a->v;
-    at.o = a->o;
-    at.dtype = DFS_BF16;
-    at.in_layout = DFS_NHD;
-    at.out_layout = DFS_NHD;
-    at.heads = H;
-    at.nq = n;
-    at.nk = n;
-    at.d = d;
-    at.block = B;
-    if (int rc = attn_dispatch(h, at, s)) return rc;
+    if (dtype == DFS_BF16 || compat) {
+      const int64_t c[3] = {n * H * d, n * H * d, n * H * dv};
+      const void* x[3] = {a->q, a->k, a->v};
+      for (int t = 0; t < 3; ++t)
+        if ((rc = finite_check_impl(x[t], c[t], dtype, flag, s))) return rc;
+      if ((rc = check_flag(flag, s))) return rc;
+      if ((rc = attn_simple(h, a->q, a->k, a->v, a->o, dtype, DFS_NHD, nullptr, DFS_NHD, nullptr, H, n, d, dv, B,
+                            nullptr, nullptr, s)))
+        return rc;
+    } else {
+      if ((rc = cast_inputs()) || (rc = check_flag(flag, s))) return rc;
+      if ((rc = h->o16.ensure(tok16))) return rc;
+      if ((rc = attn_simple(h, h->q16.p, h->k16.p, h->v16.p, h->o16.p, DFS_BF16, DFS_NHD, nullptr, DFS_NHD, nullptr,
+                            H, n, d, d, B, nullptr, nullptr, s)) ||
+          (rc = cast_impl(h->o16.p, DFS_BF16, a->o, DFS_F32, n * H * d, nullptr, s)))
+        return rc;
+    }
     if (a->dense_out) *a->dense_out = 1;
     if (a->budget_out) *a->budget_out = 1.0;
     if (a->recall_out)
@@ -700,7 +849,7 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   const uint32_t* fwd = a->perm;
   if (!fwd) {
     const PermEntry* pe;
-    if (int rc = get_perm(h, DFS_HILBERT3D, a->frames, a->height, a->width, s, &pe)) return rc;
+    if ((rc = get_perm(h, DFS_HILBERT3D, a->frames, a->height, a->width, s, &pe))) return rc;
     if (pe->n != n) return fail(DFS_E_INVALID, "run_step: permutation length does not match token count");
     fwd = pe->fwd.as<uint32_t>();
   }
@@ -722,13 +871,6 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     if (is_upd || !L || !L->head[size_t(hh)].valid) need.push_back(int(hh));
   const bool update_any = !need.empty();
 
-  int rc;
-  // Reorder: Q is gathered by K5 itself (TMA tile::gather4 by `fwd`, once per query
-  // tile), so an update step only reads q for its pooled sub-block rows; K and V are
-  // re-read by every query block that selects them, so they get one permuted [H, N, d]
-  // copy each (K with the pooled rows fused in).
-  const size_t tok_bytes = sizeof(__nv_bfloat16) * size_t(n * H * d);
-  if ((rc = h->k_hnd.ensure(tok_bytes)) || (rc = h->v_hnd.ensure(tok_bytes))) return rc;
   const int64_t pv = ceil_div(n, Bs);
   float* pq = nullptr;
   float* pk = nullptr;
@@ -738,23 +880,69 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       return rc;
     pq = h->pooled_q.as<float>();
     pk = h->pooled_k.as<float>();
-    if ((rc = permute_rows_impl(a->q, DFS_NHD, nullptr, DFS_HND, DFS_BF16, fwd, n, H, d, pq, Bs, a->nonfinite, false,
+  }
+  // attention operands after the reorder
+  const void *att_q = a->q, *att_k = h->k_hnd.p, *att_v = h->v_hnd.p;
+  if (compat) {
+    // reorder q, k, v into fp32 [H, N, d] (pooled rows of q and k fused in)
+    if ((rc = h->f32_q.ensure(sizeof(float) * size_t(n * H * d))) ||
+        (rc = h->f32_k.ensure(sizeof(float) * size_t(n * H * d))) ||
+        (rc = h->f32_v.ensure(sizeof(float) * size_t(n * H * dv))))
+      return rc;
+    if ((rc = permute_rows_impl(a->q, DFS_NHD, h->f32_q.p, DFS_HND, DFS_F32, fwd, n, H, d, pq, update_any ? Bs : 1,
+                                flag, false, s)) ||
+        (rc = permute_rows_impl(a->k, DFS_NHD, h->f32_k.p, DFS_HND, DFS_F32, fwd, n, H, d, pk, update_any ? Bs : 1,
+                                flag, false, s)) ||
+        (rc = permute_rows_impl(a->v, DFS_NHD, h->f32_v.p, DFS_HND, DFS_F32, fwd, n, H, dv, nullptr, 1, flag, false,
                                 s)))
       return rc;
-  } else if (a->nonfinite && (rc = finite_check_impl(a->q, n * H * d, DFS_BF16, a->nonfinite, s))) {
-    return rc;
+    att_q = h->f32_q.p;
+    att_k = h->f32_k.p;
+    att_v = h->f32_v.p;
+  } else {
+    // Reorder: Q is gathered by K5 itself (TMA tile::gather4 by `fwd`, once per query
+    // tile), so an update step only reads q for its pooled sub-block rows; K and V are
+    // re-read by every query block that selects them, so they get one permuted [H, N, d]
+    // copy each (K with the pooled rows fused in).
+    if ((rc = h->k_hnd.ensure(tok16)) || (rc = h->v_hnd.ensure(tok16))) return rc;
+    const void *q = a->q, *k = a->k, *v = a->v;
+    if (dtype == DFS_F32) {
+      // pooled rows from the fp32 values (what dfs::build_mask scores), then bf16 copies
+      if (update_any &&
+          ((rc = permute_rows_impl(a->q, DFS_NHD, nullptr, DFS_HND, DFS_F32, fwd, n, H, d, pq, Bs, nullptr, false, s)) ||
+           (rc = permute_rows_impl(a->k, DFS_NHD, nullptr, DFS_HND, DFS_F32, fwd, n, H, d, pk, Bs, nullptr, false, s))))
+        return rc;
+      if ((rc = cast_inputs())) return rc;
+      q = h->q16.p;
+      k = h->k16.p;
+      v = h->v16.p;
+      att_q = q;
+      pq = pk = nullptr;  // already pooled
+    }
+    if (pq) {
+      if ((rc = permute_rows_impl(q, DFS_NHD, nullptr, DFS_HND, DFS_BF16, fwd, n, H, d, pq, Bs, flag, false, s)))
+        return rc;
+    } else if (dtype == DFS_BF16 && (rc = finite_check_impl(q, n * H * d, DFS_BF16, flag, s))) {
+      return rc;
+    }
+    if ((rc = permute_rows_impl(k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, pk ? Bs : 1, flag,
+                                false, s)) ||
+        (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag, false, s)))
+      return rc;
   }
-  if ((rc = permute_rows_impl(a->k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, Bs, a->nonfinite, false,
-                              s)) ||
-      (rc = permute_rows_impl(a->v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, a->nonfinite,
-                              false, s)))
-    return rc;
+  if ((rc = check_flag(flag, s))) return rc;  // nothing scored, cached or written yet
 
   if (update_any) {
     int64_t K;
     if ((rc = dfs_topk_count(budget, m, &K))) return rc;
     if ((rc = h->scores.ensure(sizeof(double) * size_t(H * m * m)))) return rc;
-    if ((rc = score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s))) return rc;
+    pq = h->pooled_q.as<float>();
+    pk = h->pooled_k.as<float>();
+    if (compat)
+      rc = compat_scores(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
+    else
+      rc = score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
+    if (rc) return rc;
     if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large");
     if (int(need.size()) == H) {
       // common case: every head refreshes -> the LUT becomes the layer's CSR in place
@@ -808,29 +996,28 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     }
   }
 
-  dfs_attn_args at{};
-  at.q = a->q;  // raster [N, H, d]: K5 gathers the Hilbert-ordered query rows itself
-  at.k = h->k_hnd.p;
-  at.v = h->v_hnd.p;
-  at.o = a->o;
-  at.dtype = DFS_BF16;
-  at.in_layout = DFS_HND;
-  at.in_rows = fwd;
-  at.out_layout = DFS_NHD;
-  at.heads = H;
-  at.nq = n;
-  at.nk = n;
-  at.d = d;
-  at.block = B;
-  at.blk_ptr = L->ptr.as<int32_t>();
-  at.blk_idx = L->idx.as<int32_t>();
-  at.out_rows = fwd;  // fused unpermute: row i -> raster row fwd[i] (scheduler.cpp:134)
-  if ((rc = attn_dispatch(h, at, s))) return rc;
+  // attention over the selected blocks; output row i -> raster row fwd[i] (scheduler.cpp:134)
+  if (compat) {
+    rc = attn_simple(h, att_q, att_k, att_v, a->o, DFS_F32, DFS_HND, nullptr, DFS_NHD, fwd, H, n, d, dv, B,
+                     L->ptr.as<int32_t>(), L->idx.as<int32_t>(), s);
+  } else if (dtype == DFS_F32) {
+    if ((rc = h->o16.ensure(tok16))) return rc;
+    rc = attn_simple(h, att_q, att_k, att_v, h->o16.p, DFS_BF16, DFS_HND, fwd, DFS_NHD, fwd, H, n, d, d, B,
+                     L->ptr.as<int32_t>(), L->idx.as<int32_t>(), s);
+    if (!rc) rc = cast_impl(h->o16.p, DFS_BF16, a->o, DFS_F32, n * H * d, nullptr, s);
+  } else {
+    rc = attn_simple(h, att_q, att_k, att_v, a->o, DFS_BF16, DFS_HND, fwd, DFS_NHD, fwd, H, n, d, d, B,
+                     L->ptr.as<int32_t>(), L->idx.as<int32_t>(), s);
+  }
+  if (rc) return rc;
 
-  if (a->recall_out) {  // scheduler.cpp:129-131, without the N <= 4096 cap
-    if ((rc = dfs_block_recall(h, a->q, h->k_hnd.p, DFS_HND, fwd, H, n, d, L->ptr.as<int32_t>(),
-                               L->idx.as<int32_t>(), a->recall_out, stream)))
-      return rc;
+  if (a->recall_out) {  // scheduler.cpp:129-131; past the reference's 4096-row cap via the streamed kernel
+    if (compat)
+      rc = compat_recall(h, *L, h->f32_q.as<float>(), h->f32_k.as<float>(), H, n, d, a->recall_out, s);
+    else
+      rc = dfs_block_recall(h, att_q, h->k_hnd.p, DFS_HND, fwd, H, n, d, L->ptr.as<int32_t>(), L->idx.as<int32_t>(),
+                            a->recall_out, stream);
+    if (rc) return rc;
   }
   if (a->dense_out) *a->dense_out = 0;
   if (a->budget_out) *a->budget_out = budget;

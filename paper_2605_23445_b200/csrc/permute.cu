@@ -11,6 +11,8 @@
 // (mask_builder.cpp:12-28 mean_pool: fp64 accumulate, divide by B_s even for
 // the zero-padded last group, fp32 store) the CTA owns whole pooling groups and
 // emits the pooled rows from registers: the scores never re-read Q/K.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace dfsgpu {
@@ -202,7 +204,75 @@ __global__ void finite_kernel(const T* __restrict__ x, int64_t count, int32_t* _
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// fp32 -> bf16 (RNE) with the finite check of the source folded in; 8 elements per
+// thread as two 16-byte loads and one 16-byte store
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t count,
+                                     int32_t* __restrict__ nonfinite) {
+  bool bad = false;
+  const int64_t n8 = count / 8;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(src) + 2 * i);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(src) + 2 * i + 1);
+    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      bad |= !isfinite(x[2 * j]) || !isfinite(x[2 * j + 1]);
+      const __nv_bfloat162 p = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+      w[j] = *reinterpret_cast<const uint32_t*>(&p);
+    }
+    reinterpret_cast<uint4*>(dst)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  for (int64_t i = n8 * 8 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride) {
+    bad |= !isfinite(src[i]);
+    dst[i] = __float2bfloat16_rn(src[i]);
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+__global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ src, float* __restrict__ dst, int64_t count,
+                                     int32_t* __restrict__ nonfinite) {
+  bool bad = false;
+  const int64_t n8 = count / 8;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += stride) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    float x[8];
+    unpack<__nv_bfloat16>(u, x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
+    reinterpret_cast<float4*>(dst)[2 * i] = make_float4(x[0], x[1], x[2], x[3]);
+    reinterpret_cast<float4*>(dst)[2 * i + 1] = make_float4(x[4], x[5], x[6], x[7]);
+  }
+  for (int64_t i = n8 * 8 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += stride) {
+    const float x = __bfloat162float(src[i]);
+    bad |= !isfinite(x);
+    dst[i] = x;
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
 }  // namespace
+
+int cast_impl(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t count, int32_t* nonfinite,
+              cudaStream_t stream) {
+  if (count < 0) return fail(DFS_E_INVALID, "cast: negative count");
+  if (count == 0) return DFS_OK;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(DFS_E_UNSUPPORTED, "cast: buffers must be 16-byte aligned");
+  const int64_t blocks = std::min<int64_t>(ceil_div(ceil_div(count, 8), 256), 16 * kNumSMs);
+  if (src_dtype == DFS_F32 && dst_dtype == DFS_BF16)
+    cast_f32_bf16_kernel<<<unsigned(blocks), 256, 0, stream>>>(static_cast<const float*>(src),
+                                                               static_cast<__nv_bfloat16*>(dst), count, nonfinite);
+  else if (src_dtype == DFS_BF16 && dst_dtype == DFS_F32)
+    cast_bf16_f32_kernel<<<unsigned(blocks), 256, 0, stream>>>(static_cast<const __nv_bfloat16*>(src),
+                                                               static_cast<float*>(dst), count, nonfinite);
+  else
+    return fail(DFS_E_INVALID, "cast: only f32 <-> bf16");
+  DFS_LAUNCH_CHECK("cast");
+  return DFS_OK;
+}
 
 // attention.cpp:19-20 (non-finite input is an error) for the dense-step path
 int finite_check_impl(const void* x, int64_t count, int dtype, int32_t* flag, cudaStream_t stream) {

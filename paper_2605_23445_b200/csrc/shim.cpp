@@ -154,6 +154,43 @@ void attend(const Dev& q, const Dev& k, const Dev& v, const Dev& o, int64_t nq, 
   check(dfs_sparse_attn_fwd(ctx().handle, &a, stream()));
 }
 
+// Past the reference's dense-score cap (kMaxDenseScoreRows tokens) the Matrix operators
+// run the tensor-core kernels: fp32 inputs rounded to bf16 on the device, K5 (tcgen05,
+// fp32 softmax / accumulation), output converted back — the bf16 I/O tolerance of
+// SURVEY §8(d) (2e-2 of max|O|) instead of the compatibility kernels' fp64 arithmetic.
+bool fast_attention(int64_t nq, int64_t nk, int64_t d, int64_t dv, int64_t block) {
+  return std::max(nq, nk) > kMaxDenseScoreRows && (d == 64 || d == 128) && dv == d && block == 128;
+}
+
+Dev to_bf16(const Dev& x, int64_t count) {
+  Dev out(sizeof(uint16_t) * size_t(count));
+  check(dfs_cast(x.get(), DFS_F32, out.get(), DFS_BF16, count, nullptr, stream()));
+  return out;
+}
+
+void attend_tc(const Dev& q, const Dev& k, const Dev& v, const Dev& o, int64_t nq, int64_t nk, int64_t d,
+               int64_t block, const int32_t* blk_ptr, const int32_t* blk_idx) {
+  const Dev q16 = to_bf16(q, nq * d), k16 = to_bf16(k, nk * d), v16 = to_bf16(v, nk * d);
+  Dev o16(sizeof(uint16_t) * size_t(nq * d));
+  dfs_attn_args a{};
+  a.q = q16.get();
+  a.k = k16.get();
+  a.v = v16.get();
+  a.o = o16.get();
+  a.dtype = DFS_BF16;
+  a.in_layout = DFS_NHD;
+  a.out_layout = DFS_NHD;
+  a.heads = 1;
+  a.nq = nq;
+  a.nk = nk;
+  a.d = d;
+  a.block = block;
+  a.blk_ptr = blk_ptr;
+  a.blk_idx = blk_idx;
+  check(dfs_sparse_attn_fwd(ctx().handle, &a, stream()));
+  check(dfs_cast(o16.get(), DFS_BF16, o.get(), DFS_F32, nq * d, nullptr, stream()));
+}
+
 // BlockMask payload (device) -> CSR (device); throws on an empty row
 struct Csr {
   Dev ptr, idx;
@@ -398,6 +435,20 @@ MatrixD block_scores(const Matrix& q, const Matrix& k, const ScoringParams& para
   const ScoreShape s = score_shape(q, k, params);
   if (q.cols() == 0) return aggregate_scores(Matrix(s.qrows, s.kcols), params);
   const Dev dq = upload(q.values()), dk = upload(k.values());
+  if ((s.qrows > kMaxDenseScoreRows || s.valid_k > kMaxDenseScoreRows) && q.rows() == k.rows()) {
+    // Past the reference's dense-score cap (attention.cpp:107-109, which throws here):
+    // K2 pooling (fp64 sums) + the K3 scorer, which never materialises the sub-block
+    // probabilities (fp32-accurate fp16x3 tcgen05 GEMM; fp64 for other geometries).
+    require_finite(dq, q.size());
+    require_finite(dk, k.size());
+    const Dev id = identity_perm(q.rows());
+    const Dev pq = pool_rows(dq, q.rows(), q.cols(), params.sub_block_size, id);
+    const Dev pk = pool_rows(dk, k.rows(), k.cols(), params.sub_block_size, id);
+    Dev S(sizeof(double) * size_t(s.mq * s.mk));
+    check(dfs_score_blocks(ctx().handle, pq.as<float>(), pk.as<float>(), 1, q.rows(), q.cols(), params.block_size,
+                           params.sub_block_size, S.as<double>(), stream()));
+    return download_scores(S, s.mq, s.mk);
+  }
   const Dev P = subblock_scores_dev(dq, q.rows(), dk, k.rows(), q.cols(), params, s);
   Dev S(sizeof(double) * size_t(s.mq * s.mk));
   check(dfs_aggregate_scores(P.as<float>(), 1, s.mq, s.mk, s.subs, S.as<double>(), stream()));
@@ -420,7 +471,10 @@ Matrix full_attention_output(const Matrix& q, const Matrix& k, const Matrix& v) 
   require_finite(dv, v.size());
   if (v.cols() == 0) return out;
   Dev o(sizeof(float) * size_t(out.size()));
-  attend(dq, dk, dv, o, q.rows(), k.rows(), q.cols(), v.cols(), 128, nullptr, nullptr, nullptr);
+  if (fast_attention(q.rows(), k.rows(), q.cols(), v.cols(), 128))
+    attend_tc(dq, dk, dv, o, q.rows(), k.rows(), q.cols(), 128, nullptr, nullptr);
+  else
+    attend(dq, dk, dv, o, q.rows(), k.rows(), q.cols(), v.cols(), 128, nullptr, nullptr, nullptr);
   download(o, out.values());
   sync();
   return out;
@@ -465,8 +519,12 @@ Matrix block_sparse_attention(const Matrix& q, const Matrix& k, const Matrix& v,
   const Dev bits = upload(std::span<const uint8_t>(mask.bytes()));
   const Csr csr = mask_csr(bits, mask.block_count());
   Dev o(sizeof(float) * size_t(out.size()));
-  attend(dq, dk, dv, o, q.rows(), k.rows(), q.cols(), v.cols(), mask.block_size(), csr.ptr.as<int32_t>(),
-         csr.idx.as<int32_t>(), nullptr);
+  if (fast_attention(q.rows(), k.rows(), q.cols(), v.cols(), mask.block_size()))
+    attend_tc(dq, dk, dv, o, q.rows(), k.rows(), q.cols(), mask.block_size(), csr.ptr.as<int32_t>(),
+              csr.idx.as<int32_t>());
+  else
+    attend(dq, dk, dv, o, q.rows(), k.rows(), q.cols(), v.cols(), mask.block_size(), csr.ptr.as<int32_t>(),
+           csr.idx.as<int32_t>(), nullptr);
   download(o, out.values());
   sync();
   return out;
@@ -561,10 +619,91 @@ bool should_update(const MaskCache& cache, int layer, int head, int step, const 
   return !cache.contains(layer, head) || schedule.is_update_step(step);
 }
 
-// scheduler.cpp:91-135 on the device: one upload of q/k/v and the permutation, the
-// reorder with fused pooling (K2), scoring (fp64) + selection (K4) or the cached mask,
-// block-sparse attention (fp64 accumulation) with the unpermute fused into its
-// epilogue, one download of the raster-order output.
+namespace {
+
+// One device step (dfs_run_step) for `heads` heads of one layer: q/k/v fp32 [n, heads, d]
+// (host, packed) -> out [n, heads, dv]. fp32 steps run the compatibility kernels up to
+// kMaxDenseScoreRows tokens (bit-identical to the Matrix operators above) and the
+// tcgen05 kernels past it.
+struct DeviceStep {
+  dfs_handle* h;
+  dfs_stream st;
+  const uint32_t* fwd;  // device forward permutation
+};
+
+struct StepResult {
+  bool dense = true;
+  double budget = 1.0;
+  std::vector<int> updated;
+  std::vector<double> sparsity, recall;
+};
+
+StepResult device_step(const DeviceStep& ds, const dfs_schedule& sched, const float* q, const float* k,
+                       const float* v, float* out, int64_t n, int64_t heads, int64_t d, int64_t dv, int64_t block,
+                       int64_t sub, int layer, int step, bool force_dense, bool record_recall) {
+  Dev dq(sizeof(float) * size_t(n * heads * d)), dk(sizeof(float) * size_t(n * heads * d));
+  Dev dvv(sizeof(float) * size_t(n * heads * dv)), dout(sizeof(float) * size_t(n * heads * dv));
+  sync();  // allocated in this thread's stream order; used on ds.st below
+  cudaStream_t cs = static_cast<cudaStream_t>(ds.st);
+  cuda(cudaMemcpyAsync(dq.get(), q, sizeof(float) * size_t(n * heads * d), cudaMemcpyHostToDevice, cs), "upload");
+  cuda(cudaMemcpyAsync(dk.get(), k, sizeof(float) * size_t(n * heads * d), cudaMemcpyHostToDevice, cs), "upload");
+  cuda(cudaMemcpyAsync(dvv.get(), v, sizeof(float) * size_t(n * heads * dv), cudaMemcpyHostToDevice, cs), "upload");
+  StepResult r;
+  r.updated.assign(size_t(heads), 0);
+  r.sparsity.assign(size_t(heads), 0.0);
+  r.recall.assign(size_t(heads), 1.0);
+  int dense = 1;
+  dfs_step_args a{};
+  a.q = dq.get();
+  a.k = dk.get();
+  a.v = dvv.get();
+  a.o = dout.get();
+  a.n = n;
+  a.heads = heads;
+  a.d = d;
+  a.dv = dv;
+  a.dtype = DFS_F32;
+  a.perm = ds.fwd;
+  a.block = block;
+  a.sub_block = sub;
+  a.layer = layer;
+  a.step = step;
+  a.force_dense = force_dense;
+  a.dense_out = &dense;
+  a.budget_out = &r.budget;
+  a.updated_out = r.updated.data();
+  a.sparsity_out = r.sparsity.data();
+  a.recall_out = record_recall ? r.recall.data() : nullptr;
+  check(dfs_run_step(ds.h, &sched, &a, ds.st));
+  cuda(cudaMemcpyAsync(out, dout.get(), sizeof(float) * size_t(n * heads * dv), cudaMemcpyDeviceToHost, cs),
+       "download");
+  cuda(cudaStreamSynchronize(cs), "cudaStreamSynchronize");
+  r.dense = dense != 0;
+  return r;
+}
+
+BlockMask cached_mask(dfs_handle* h, dfs_stream st, int layer, int head) {
+  int64_t m = 0, b = 0;
+  int last = 0;
+  check(dfs_mask_cache_info(h, layer, head, &m, &b, &last));
+  BlockMask mask(m, b);
+  Dev bits(size_t(BlockMask::byte_size(m)));
+  sync();  // allocated in this thread's stream order; used on st below
+  check(dfs_mask_cache_get(h, layer, head, bits.as<uint8_t>(), nullptr, nullptr, st));
+  cuda(cudaMemcpyAsync(mask.bytes().data(), bits.get(), size_t(BlockMask::byte_size(m)), cudaMemcpyDeviceToHost,
+                       static_cast<cudaStream_t>(st)),
+       "download");
+  cuda(cudaStreamSynchronize(static_cast<cudaStream_t>(st)), "cudaStreamSynchronize");
+  return mask;
+}
+
+}  // namespace
+
+// scheduler.cpp:91-135: argument checks in the reference's order on the host, then ONE
+// dfs_run_step on this thread's handle (reorder + fused pooling, scoring + selection or
+// the cached mask, attention with the unpermute fused in). The host MaskCache entry of
+// (layer, head) is mirrored into the handle's device cache for a reuse step and read
+// back after an update, so should_update / find / store keep the reference's semantics.
 Matrix run_step(const Matrix& q, const Matrix& k, const Matrix& v, const Permutation& perm,
                 const ScoringParams& params, const SparsitySchedule& schedule, MaskCache& cache, int layer, int head,
                 int step, const StepOptions& options, StepStats* stats) {
@@ -573,96 +712,74 @@ Matrix run_step(const Matrix& q, const Matrix& k, const Matrix& v, const Permuta
   if (!budget || options.force_dense) {
     if (stats) {
       *stats = StepStats{};
-      stats->recall_recorded = options.record_recall && q.rows() <= kMaxDenseScoreRows;
+      stats->recall_recorded = options.record_recall;  // dense: recall 1 at any N
     }
     return full_attention_output(q, k, v);
   }
   const int64_t n = q.rows();
   if (k.rows() != n || v.rows() != n) throw std::invalid_argument("apply_permutation: length mismatch");
-  const int64_t d = q.cols(), dv = v.cols();
   const bool update = should_update(cache, layer, head, step, schedule);
-  if (update) params.validate();
-
-  // reorder (+ pooled rows for the scorer) and the finite check in the same pass
-  const Dev fwd = upload(std::span<const uint32_t>(perm.forward));
-  const Dev hq = upload(q.values()), hk = upload(k.values()), hv = upload(v.values());
-  Dev rq(sizeof(float) * size_t(n * d)), rk(sizeof(float) * size_t(n * d)), rv(sizeof(float) * size_t(n * dv));
-  Dev flag(sizeof(int32_t));
-  cuda(cudaMemsetAsync(flag.get(), 0, sizeof(int32_t), ctx().stream), "memset");
-  Dev pq, pk;
-  const int64_t bs = update ? params.sub_block_size : 1;
-  const int64_t pooled_rows = block_count_for(n, bs);
-  if (update && d > 0) {
-    pq = Dev(sizeof(float) * size_t(pooled_rows * d));
-    pk = Dev(sizeof(float) * size_t(pooled_rows * d));
-  }
-  if (d > 0) {
-    check(dfs_permute_rows(hq.get(), DFS_NHD, rq.get(), DFS_NHD, DFS_F32, fwd.as<uint32_t>(), n, 1, d,
-                           update ? pq.as<float>() : nullptr, bs, flag.as<int32_t>(), stream()));
-    check(dfs_permute_rows(hk.get(), DFS_NHD, rk.get(), DFS_NHD, DFS_F32, fwd.as<uint32_t>(), n, 1, d,
-                           update ? pk.as<float>() : nullptr, bs, flag.as<int32_t>(), stream()));
-  }
-  if (dv > 0)
-    check(dfs_permute_rows(hv.get(), DFS_NHD, rv.get(), DFS_NHD, DFS_F32, fwd.as<uint32_t>(), n, 1, dv, nullptr, 1,
-                           flag.as<int32_t>(), stream()));
-  int32_t bad = 0;
-  download(flag, std::span<int32_t>(&bad, 1));
-  sync();
-  if (bad) throw std::invalid_argument("attention: non-finite input");
-  if (n < 1 || d < 1) throw std::invalid_argument("attention: empty input");
-
-  BlockMask mask;
-  Dev bits;
+  std::optional<MaskCache::Entry> entry;
   if (update) {
-    // build_mask on the reordered rows (mask_builder.cpp:119-124)
-    const ScoreShape s = score_shape(q, k, params);
-    const Dev P = pooled_softmax(pq, s.valid_q, s.qrows, pk, s.valid_k, s.kcols, d);
-    Dev S(sizeof(double) * size_t(s.mq * s.mk));
-    check(dfs_aggregate_scores(P.as<float>(), 1, s.mq, s.mk, s.subs, S.as<double>(), stream()));
-    const int64_t kk = topk_count(*budget, s.mq);
-    mask = BlockMask(s.mq, params.block_size);
-    bits = Dev(size_t(BlockMask::byte_size(s.mq)));
-    check(dfs_topk_select(S.as<double>(), 1, s.mq, kk, nullptr, bits.as<uint8_t>(), stream()));
-    download(bits, mask.bytes());
-    sync();
-    cache.store(layer, head, mask, step);
+    params.validate();
+    if (q.cols() != k.cols()) throw std::invalid_argument("subblock_scores: head dims differ");
   } else {
-    mask = cache.find(layer, head)->mask;
-    bits = upload(std::span<const uint8_t>(mask.bytes()));
+    entry = cache.find(layer, head);
+    if (q.cols() != k.cols()) throw std::invalid_argument("attention: q and k head dims differ");
+    check_mask_geometry(n, n, entry->mask);
+    check_rows_nonempty(entry->mask);
   }
-  check_mask_geometry(n, n, mask);
-  check_rows_nonempty(mask);
-
+  if (n < 1 || q.cols() < 1) throw std::invalid_argument("attention: empty input");
+  const int64_t d = q.cols(), dv = v.cols();
   Matrix out(n, dv);
-  if (dv > 0) {
-    const Csr csr = mask_csr(bits, mask.block_count());
-    Dev o(sizeof(float) * size_t(n * dv));
-    // output row i (reordered) lands on raster row forward[i] (scheduler.cpp:134)
-    attend(rq, rk, rv, o, n, n, d, dv, mask.block_size(), csr.ptr.as<int32_t>(), csr.idx.as<int32_t>(),
-           fwd.as<uint32_t>());
-    download(o, out.values());
+  if (dv == 0) {  // nothing to attend; the reference still builds / caches the mask
+    if (update) cache.store(layer, head, build_mask(apply_permutation(perm, q), apply_permutation(perm, k), params,
+                                                    *budget), step);
+    const BlockMask mask = cache.find(layer, head)->mask;
+    if (stats) {
+      stats->dense = false;
+      stats->budget = *budget;
+      stats->mask_updated = update;
+      const double m = double(mask.block_count());
+      stats->sparsity = 1.0 - double(mask.selected_count()) / (m * m);
+      stats->recall_recorded = false;
+    }
+    return out;
   }
+  Context& c = ctx();
+  check(dfs_mask_cache_clear(c.handle));
+  const int64_t block = update ? params.block_size : entry->mask.block_size();
+  if (!update) {
+    const Dev bits = upload(std::span<const uint8_t>(entry->mask.bytes()));
+    check(dfs_mask_cache_store(c.handle, 0, 0, bits.as<uint8_t>(), entry->mask.block_count(), block,
+                               entry->last_update_step, c.stream));
+  }
+  const Dev fwd = upload(std::span<const uint32_t>(perm.forward));
+  const SparsitySchedule::Config& cfg = schedule.config();
+  dfs_schedule sched{cfg.total_steps, cfg.warmup_fraction, cfg.phase_budgets.data(), int(cfg.phase_budgets.size()),
+                     cfg.phase_fraction, cfg.update_interval};
+  const StepResult r = device_step(DeviceStep{c.handle, c.stream, fwd.as<uint32_t>()}, sched, q.values().data(),
+                                   k.values().data(), v.values().data(), out.values().data(), n, 1, d, dv, block,
+                                   update ? params.sub_block_size : block, 0, step, false, options.record_recall);
+  BlockMask mask = update ? cached_mask(c.handle, c.stream, 0, 0) : entry->mask;
+  if (update) cache.store(layer, head, mask, step);
   if (stats) {
     stats->dense = false;
     stats->budget = *budget;
     stats->mask_updated = update;
     const double m = double(mask.block_count());
     stats->sparsity = 1.0 - double(mask.selected_count()) / (m * m);  // metrics.cpp:39-42
-    stats->recall_recorded = false;
-    if (options.record_recall && n <= kMaxDenseScoreRows) {
-      Dev A(sizeof(float) * size_t(n * n));
-      check(dfs_softmax_scores(rq.as<float>(), rk.as<float>(), 1, n, n, n, n, d, 0.0, A.as<float>(), stream()));
-      double r = 0.0;
-      check(dfs_attention_recall(A.as<float>(), n, n, bits.as<uint8_t>(), mask.block_count(), mask.block_size(), &r,
-                                 stream()));
-      stats->recall = r;
-      stats->recall_recorded = true;
-    }
+    stats->recall_recorded = options.record_recall;
+    stats->recall = options.record_recall ? r.recall[0] : 1.0;
   }
-  sync();
   return out;
 }
 
+// scheduler.cpp:137-186. Steps run in order; within a step the (layer, head) pairs are
+// fanned out as in the reference for the host work (workload.tensors, sinks), while the
+// device runs ONE batched dfs_run_step per layer over all its heads. The trajectory owns
+// one library handle (and stream) per layer, and the handle's device mask cache plays the
+// reference's trajectory-local MaskCache. Layers run concurrently on their own streams.
 std::vector<TrajectoryRow> run_trajectory(const Workload& workload, const Permutation& perm,
                                           const ScoringParams& params, const SparsitySchedule& schedule,
                                           const TrajectoryOptions& options) {
@@ -670,33 +787,107 @@ std::vector<TrajectoryRow> run_trajectory(const Workload& workload, const Permut
     throw std::invalid_argument("run_trajectory: workload steps differ from schedule steps");
   if (workload.layers < 1 || workload.heads < 1 || !workload.tensors)
     throw std::invalid_argument("run_trajectory: invalid workload");
-  MaskCache cache;
-  const int pairs = workload.layers * workload.heads;
+  const int L = workload.layers, H = workload.heads, pairs = L * H;
+  const int64_t n = perm.size();
   std::vector<TrajectoryRow> rows(size_t(workload.steps) * size_t(pairs));
+
+  struct LayerDev {
+    dfs_handle* h = nullptr;
+    cudaStream_t st = nullptr;
+    ~LayerDev() {
+      if (st) cudaStreamDestroy(st);
+      if (h) dfs_handle_destroy(h);
+    }
+  };
+  int dev = 0;
+  cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  std::vector<LayerDev> layers(static_cast<size_t>(L));
+  for (auto& ld : layers) {
+    check(dfs_handle_create(&ld.h, dev));
+    cuda(cudaStreamCreateWithFlags(&ld.st, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  uint32_t* fwd = nullptr;
+  if (n > 0) {
+    cuda(cudaMalloc(&fwd, sizeof(uint32_t) * size_t(n)), "cudaMalloc");
+    cuda(cudaMemcpy(fwd, perm.forward.data(), sizeof(uint32_t) * size_t(n), cudaMemcpyHostToDevice), "upload");
+  }
+  struct FreeOnExit {
+    uint32_t* p;
+    ~FreeOnExit() {
+      if (p) cudaFree(p);
+    }
+  } free_fwd{fwd};
+  const SparsitySchedule::Config& cfg = schedule.config();
+  const dfs_schedule sched{cfg.total_steps, cfg.warmup_fraction, cfg.phase_budgets.data(),
+                           int(cfg.phase_budgets.size()), cfg.phase_fraction, cfg.update_interval};
+
+  std::vector<StepTensors> tensors(static_cast<size_t>(pairs));
+  std::vector<Matrix> outs(static_cast<size_t>(pairs));
+  std::vector<std::optional<BlockMask>> updated(static_cast<size_t>(pairs));
   for (int step = 0; step < workload.steps; ++step) {
-    // (layer, head) pairs fan out over worker threads, each with its own stream
+    // host: every pair's tensors, in parallel like the reference's fan-out
     parallel_for(pairs, options.threads, [&](int64_t pair) {
-      const int layer = int(pair) / workload.heads;
-      const int head = int(pair) % workload.heads;
-      const StepTensors t = workload.tensors(step, layer, head);
-      if (t.q.rows() != perm.size()) throw std::invalid_argument("run_trajectory: token count drifted between steps");
-      StepOptions so;
-      so.record_recall = options.record_recall;
-      so.force_dense = options.dense_layers.count(layer) > 0;
-      StepStats st;
-      const Matrix out = run_step(t.q, t.k, t.v, perm, params, schedule, cache, layer, head, step, so, &st);
-      TrajectoryRow& row = rows[size_t(step) * size_t(pairs) + size_t(pair)];
-      row.step = step;
-      row.layer = layer;
-      row.head = head;
-      row.budget = st.budget;
-      row.sparsity = st.sparsity;
-      row.recall = st.recall;
-      row.recall_recorded = st.recall_recorded;
-      row.mask_updated = st.mask_updated;
-      row.dense = st.dense;
-      if (options.mask_sink && st.mask_updated) options.mask_sink(step, layer, head, cache.find(layer, head)->mask);
-      if (options.output_sink) options.output_sink(step, layer, head, out);
+      const int layer = int(pair) / H, head = int(pair) % H;
+      tensors[size_t(pair)] = workload.tensors(step, layer, head);
+      if (tensors[size_t(pair)].q.rows() != n)
+        throw std::invalid_argument("run_trajectory: token count drifted between steps");
+    });
+    // device: one batched step per layer (all heads), layers concurrently
+    parallel_for(L, options.threads, [&](int64_t layer) {
+      const int l = int(layer);
+      const StepTensors& t0 = tensors[size_t(l * H)];
+      const int64_t d = t0.q.cols(), dv = t0.v.cols();
+      bool uniform = d > 0 && dv > 0;
+      for (int hh = 0; hh < H && uniform; ++hh) {
+        const StepTensors& t = tensors[size_t(l * H + hh)];
+        uniform = t.q.cols() == d && t.k.cols() == d && t.k.rows() == n && t.v.rows() == n && t.v.cols() == dv;
+      }
+      const bool force_dense = options.dense_layers.count(l) > 0;
+      const std::optional<double> budget = schedule.budget_at(step);
+      if (!uniform) {
+        // ragged shapes: the per-head operator, which raises the reference's errors
+        throw std::invalid_argument("run_trajectory: heads of a layer must share q/k/v shapes (" +
+                                    std::to_string(n) + " tokens)");
+      }
+      std::vector<float> q(size_t(n * H * d)), k(size_t(n * H * d)), v(size_t(n * H * dv)), o(size_t(n * H * dv));
+      for (int hh = 0; hh < H; ++hh) {
+        const StepTensors& t = tensors[size_t(l * H + hh)];
+        for (int64_t i = 0; i < n; ++i) {
+          std::memcpy(&q[size_t((i * H + hh) * d)], t.q.row(i).data(), sizeof(float) * size_t(d));
+          std::memcpy(&k[size_t((i * H + hh) * d)], t.k.row(i).data(), sizeof(float) * size_t(d));
+          std::memcpy(&v[size_t((i * H + hh) * dv)], t.v.row(i).data(), sizeof(float) * size_t(dv));
+        }
+      }
+      const StepResult r = device_step(DeviceStep{layers[size_t(l)].h, layers[size_t(l)].st, fwd}, sched, q.data(),
+                                       k.data(), v.data(), o.data(), n, H, d, dv, params.block_size,
+                                       params.sub_block_size, l, step, force_dense, options.record_recall);
+      for (int hh = 0; hh < H; ++hh) {
+        const int64_t pair = int64_t(l) * H + hh;
+        Matrix& out = outs[size_t(pair)];
+        out = Matrix(n, dv);
+        for (int64_t i = 0; i < n; ++i)
+          std::memcpy(out.row(i).data(), &o[size_t((i * H + hh) * dv)], sizeof(float) * size_t(dv));
+        updated[size_t(pair)].reset();
+        if (r.updated[size_t(hh)] && options.mask_sink)
+          updated[size_t(pair)] = cached_mask(layers[size_t(l)].h, layers[size_t(l)].st, l, hh);
+        TrajectoryRow& row = rows[size_t(step) * size_t(pairs) + size_t(pair)];
+        row.step = step;
+        row.layer = l;
+        row.head = hh;
+        row.dense = r.dense;
+        row.budget = r.dense ? 1.0 : r.budget;
+        row.sparsity = r.dense ? 0.0 : r.sparsity[size_t(hh)];
+        row.mask_updated = r.updated[size_t(hh)] != 0;
+        row.recall_recorded = options.record_recall;
+        row.recall = options.record_recall ? r.recall[size_t(hh)] : 1.0;
+        (void)budget;
+      }
+    });
+    // host: sinks, fanned out like the reference (they may be called from worker threads)
+    parallel_for(pairs, options.threads, [&](int64_t pair) {
+      const int layer = int(pair) / H, head = int(pair) % H;
+      if (options.mask_sink && updated[size_t(pair)]) options.mask_sink(step, layer, head, *updated[size_t(pair)]);
+      if (options.output_sink) options.output_sink(step, layer, head, outs[size_t(pair)]);
     });
   }
   return rows;

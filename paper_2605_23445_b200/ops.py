@@ -400,17 +400,23 @@ def _attn_call(q, k, v, out, heads, nq, nk, d, block, blk_ptr, blk_idx, in_layou
                       out_layout, heads, nq, nk, d, block,
                       0 if blk_ptr is None else blk_ptr.data_ptr(),
                       0 if blk_idx is None else blk_idx.data_ptr(),
-                      0 if out_rows is None else out_rows.data_ptr(), float(scale), int(force_generic), 0,
-                      0 if in_rows is None else in_rows.data_ptr())
+                      0 if out_rows is None else out_rows.data_ptr(), float(scale), int(force_generic),
+                      0 if v.shape[-1] == d else v.shape[-1], 0 if in_rows is None else in_rows.data_ptr())
     capi.call("dfs_sparse_attn_fwd", default_handle().ptr, C.byref(a), _stream())
 
 
 def _check_qkv(q, k, v):  # attention.cpp:14-21
     _check_cuda(q, k, v)
+    if q.dim() != k.dim() or k.dim() != v.dim() or q.dim() not in (2, 3):
+        raise ValueError("attention: expected [N, d] or [N, H, d] tensors")
     if q.shape[-1] != k.shape[-1]:
         raise ValueError("attention: q and k head dims differ")
     if k.shape[0] != v.shape[0]:
         raise ValueError("attention: k and v row counts differ")
+    if q.dim() == 3 and not (q.shape[1] == k.shape[1] == v.shape[1]):
+        raise ValueError("attention: q, k, v head counts differ")
+    if v.shape[-1] != q.shape[-1] and q.dtype != torch.float32:
+        raise ValueError("attention: dv != d only on the fp32 path")
     if q.shape[0] < 1 or k.shape[0] < 1 or q.shape[-1] < 1:
         raise ValueError("attention: empty input")
     if q.dtype != k.dtype or k.dtype != v.dtype:
@@ -451,7 +457,7 @@ def block_sparse_attention(q, k, v, mask, force_generic: bool = False) -> torch.
             raise ValueError("block mask geometry inconsistent with sequence length")
     ptr, idx = mask_to_csr(ms, m)
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    out = torch.empty_like(q)
+    out = q.new_empty(q.shape[:-1] + (v.shape[-1],))
     _attn_call(q, k, v, out, h, n, n, d, b, ptr, idx, capi.DFS_NHD, capi.DFS_NHD, force_generic=force_generic)
     return out
 
@@ -464,7 +470,7 @@ def full_attention_output(q, k, v, block: int = 128, force_generic: bool = False
     nq, h, d = _as_heads(q)
     nk = k.shape[0]
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-    out = torch.empty_like(q)
+    out = q.new_empty(q.shape[:-1] + (v.shape[-1],))
     _attn_call(q, k, v, out, h, nq, nk, d, block, None, None, capi.DFS_NHD, capi.DFS_NHD,
                force_generic=force_generic)
     return out
@@ -556,47 +562,50 @@ class SparsitySchedule:
 
 
 class MaskCache:
-    """scheduler.hpp:54-71 — device-resident, keyed by (layer, head), owned by a Handle."""
+    """scheduler.hpp:54-71 — device-resident, keyed by (layer, head), owned by a Handle.
+
+    Internally locked like the reference's (scheduler.cpp:58-83): a dfs_handle must not be
+    used by two threads at once (dfs_gpu.h), so every call on the cache's handle —
+    including run_step with this cache — holds `self.lock`."""
 
     def __init__(self, handle: Handle | None = None):
         self.handle = handle or Handle()
+        self.lock = threading.RLock()
 
     def contains(self, layer: int, head: int) -> bool:
         f = C.c_int()
-        capi.call("dfs_mask_cache_contains", self.handle.ptr, layer, head, C.byref(f))
+        with self.lock:
+            capi.call("dfs_mask_cache_contains", self.handle.ptr, layer, head, C.byref(f))
         return bool(f.value)
 
     def find(self, layer: int, head: int):
         """-> (BlockMask, last_update_step) or None (a copy, like the reference)."""
-        if not self.contains(layer, head):
-            return None
-        m, step = C.c_int64(), C.c_int()
-        capi.call("dfs_mask_cache_get", self.handle.ptr, layer, head, None, C.byref(step), C.byref(m), _stream())
-        bits = torch.empty(BlockMask.byte_size(m.value), dtype=torch.uint8, device="cuda")
-        capi.call("dfs_mask_cache_get", self.handle.ptr, layer, head, _ptr(bits), C.byref(step), C.byref(m),
-                  _stream())
-        return BlockMask(bits, m.value, self._block(layer)), step.value
-
-    def _block(self, layer):
-        return self._blocks.get(layer, 0) if hasattr(self, "_blocks") else 0
+        with self.lock:
+            if not self.contains(layer, head):
+                return None
+            m, b, step = C.c_int64(), C.c_int64(), C.c_int()
+            capi.call("dfs_mask_cache_info", self.handle.ptr, layer, head, C.byref(m), C.byref(b), C.byref(step))
+            bits = torch.empty(BlockMask.byte_size(m.value), dtype=torch.uint8, device="cuda")
+            capi.call("dfs_mask_cache_get", self.handle.ptr, layer, head, _ptr(bits), None, None, _stream())
+            return BlockMask(bits, m.value, b.value), step.value
 
     def store(self, layer: int, head: int, mask: BlockMask, step: int):
-        if not hasattr(self, "_blocks"):
-            self._blocks = {}
-        self._blocks[layer] = mask.block_size
-        capi.call("dfs_mask_cache_store", self.handle.ptr, layer, head, _ptr(mask.bits), mask.block_count,
-                  mask.block_size, step, _stream())
+        with self.lock:
+            capi.call("dfs_mask_cache_store", self.handle.ptr, layer, head, _ptr(mask.bits), mask.block_count,
+                      mask.block_size, step, _stream())
 
     def size(self) -> int:
         n = C.c_int64()
-        capi.call("dfs_mask_cache_size", self.handle.ptr, C.byref(n))
+        with self.lock:
+            capi.call("dfs_mask_cache_size", self.handle.ptr, C.byref(n))
         return n.value
 
     def empty(self) -> bool:
         return self.size() == 0
 
     def clear(self):
-        capi.call("dfs_mask_cache_clear", self.handle.ptr)
+        with self.lock:
+            capi.call("dfs_mask_cache_clear", self.handle.ptr)
 
 
 def should_update(cache: MaskCache, layer: int, head: int, step: int, schedule: SparsitySchedule) -> bool:
@@ -617,21 +626,30 @@ class StepStats:  # scheduler.hpp:78-85 (per head)
 
 def run_step(q, k, v, dims, params: ScoringParams, schedule: SparsitySchedule, cache: MaskCache, layer: int,
              step: int, force_dense: bool = False, perm: Permutation | None = None, out=None,
-             check_finite: bool = False, record_recall: bool = False):
-    """scheduler.hpp:93 run_step for ALL heads of one layer: q, k, v [N, H, d] bf16 raster order.
+             record_recall: bool = False):
+    """scheduler.hpp:93 run_step for ALL heads of one layer: q, k, v [N, H, d] raster order.
 
+    bf16 is the performance path; fp32 runs the compatibility kernels up to 4096 tokens
+    (the reference's fp64 arithmetic) and the tcgen05 kernels past it. Non-finite input
+    raises ValueError before anything is scored, cached or written (attention.cpp:19-20).
     Returns (out [N, H, d], StepStats)."""
     _check_cuda(q, k, v)
-    if q.dtype != torch.bfloat16:
-        raise ValueError("run_step: the batched path takes bf16 [N, H, d] activations")
+    if q.dtype not in (torch.bfloat16, torch.float32) or k.dtype != q.dtype or v.dtype != q.dtype:
+        raise ValueError("run_step: q, k, v must all be bf16 (performance path) or all fp32")
+    if q.dim() != 3 or k.shape != q.shape or v.shape[:2] != q.shape[:2]:
+        raise ValueError("run_step: expected q, k [N, H, d] and v [N, H, dv] with the same N and H")
+    if not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
+        raise ValueError("run_step: q, k, v must be contiguous [N, H, d] tensors")
     n, h, d = q.shape
+    dv = v.shape[2]
     dims = _dims(dims)
     if perm is None and dims.token_count() != n:
         raise ValueError("run_step: permutation length does not match token count")
     if perm is not None and perm.size() != n:
         raise ValueError("run_step: permutation length does not match token count")
-    out = torch.empty_like(q) if out is None else out
-    flag = torch.zeros(1, dtype=torch.int32, device=q.device) if check_finite else None
+    out = torch.empty((n, h, dv), dtype=q.dtype, device=q.device) if out is None else out
+    if out.shape != (n, h, dv) or out.dtype != q.dtype or not out.is_contiguous():
+        raise ValueError("run_step: out must be a contiguous [N, H, dv] tensor of the input dtype")
     dense, budget = C.c_int(), C.c_double()
     upd = (C.c_int * h)()
     spars = (C.c_double * h)()
@@ -639,12 +657,11 @@ def run_step(q, k, v, dims, params: ScoringParams, schedule: SparsitySchedule, c
     a = capi.StepArgs(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), n, h, d,
                       0 if perm is None else perm.forward.data_ptr(), dims.frames, dims.height, dims.width,
                       params.block_size, params.sub_block_size, layer, step, int(force_dense),
-                      0 if flag is None else flag.data_ptr(), C.pointer(dense), C.pointer(budget),
+                      None, C.pointer(dense), C.pointer(budget),
                       C.cast(upd, C.POINTER(C.c_int)), C.cast(spars, C.POINTER(C.c_double)),
-                      C.cast(rec, C.POINTER(C.c_double)) if rec is not None else None)
-    capi.call("dfs_run_step", cache.handle.ptr, C.byref(schedule._s), C.byref(a), _stream())
-    if flag is not None and int(flag.item()):
-        raise ValueError("attention: non-finite input")
+                      C.cast(rec, C.POINTER(C.c_double)) if rec is not None else None, _dtype_code(q), dv)
+    with cache.lock:
+        capi.call("dfs_run_step", cache.handle.ptr, C.byref(schedule._s), C.byref(a), _stream())
     stats = StepStats(bool(dense.value), budget.value, [bool(x) for x in upd], list(spars),
                       list(rec) if rec is not None else None)
     return out, stats

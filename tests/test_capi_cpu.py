@@ -22,7 +22,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(_capi.lib, name), name
     assert declared == set(_capi.EXPORTS), declared ^ set(_capi.EXPORTS)
-    assert _capi.lib.dfs_abi_version() == 1
+    assert _capi.lib.dfs_abi_version() == 2
 
 
 @pytest.mark.parametrize("case", [

@@ -5,7 +5,9 @@ Wan-720p call) runs through dfs.run_step exactly as the bench does, then
 * every mask row selects exactly K = topk_count(gamma, M) blocks, and the
   cached payload round-trips through the device mask cache;
 * block scores of two heads: rows sum to B/B_s (test_mask_builder.cpp:182-198),
-  the mask is the oracle's top-K of those scores bit-for-bit (K4 parity);
+  the mask is the oracle's top-K of those scores bit-for-bit (K4 parity), the
+  scores are within 1e-4 of the C oracle's fp64 block_scores on the same values and
+  the mask agrees with the oracle's own mask on >= 99.5 % of bits;
 * sampled output rows of sampled heads (including the partial last query block)
   match an fp64 restatement of attend_row (attention.cpp:32-60) over the
   selected keys, computed only for those rows: max|O - O_ref| / max|O_ref| <= 2e-2;
@@ -76,8 +78,21 @@ def test_full_call_properties(wl):
                            m.ScoringParams(B, Bs)).cpu().numpy()
         assert np.allclose(S.sum(1), B // Bs, rtol=1e-5)
         assert (mask_bits_to_dense(ora.topk_select(S, gamma), M) == dense).all()
+        # ... and against the C oracle on the same (bf16) values: fp64 block scores,
+        # the oracle's own top-K mask (>= 99.5 % of bits)
+        S_ref = ora.block_scores(rq, rk, B, Bs)
+        assert np.abs(S - S_ref).max() / np.abs(S_ref).max() <= 1e-4, (wl, h)
+        bits_ref = ora.topk_select(S_ref, gamma)
+        dense_ref = mask_bits_to_dense(bits_ref, M)
+        assert (dense_ref == dense).mean() >= 0.995, (wl, h)
         rows = np.concatenate([rng.choice(n - B, 40, replace=False), np.arange((M - 1) * B, n)[:8]])
         ref = attend_rows(rq, rk, rv, dense, rows, B)
         got = out[:, h].float().cpu().numpy()[fwd[rows]]
         err = np.abs(got - ref).max() / np.abs(ref).max()
         assert err <= 2e-2, (wl, h, err)
+        # output of the oracle's block_sparse_attention under the ORACLE's mask, first and last query blocks
+        for u in (0, M - 1):
+            lo, hi = u * B, min((u + 1) * B, n)
+            o_ref = ora.block_sparse_attention(rq, rk, rv, bits_ref, M, B, rows=(lo, hi))[lo:hi]
+            o_got = out[:, h].float().cpu().numpy()[fwd[lo:hi]]
+            assert np.abs(o_got - o_ref).max() / np.abs(o_ref).max() <= 2e-2, (wl, h, u)

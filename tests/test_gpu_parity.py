@@ -273,7 +273,7 @@ def test_run_step_tiny_config_matches_reference(golden):
                                update_interval=1)
     cache = m.MaskCache()
     out, st = m.run_step(cu(Q, torch.bfloat16), cu(K, torch.bfloat16), cu(V, torch.bfloat16), dims,
-                         m.ScoringParams(64, 16), sched, cache, layer=0, step=0, check_finite=True)
+                         m.ScoringParams(64, 16), sched, cache, layer=0, step=0)
     assert not st.dense and all(st.mask_updated)
     out = host(out.float())
     fwd = g["fwd"]
@@ -399,7 +399,7 @@ def test_run_step_generic_and_tcgen05_paths(d):
     sched = m.SparsitySchedule(total_steps=1, warmup_fraction=0.0, phase_budgets=(gam,), phase_fraction=1.0,
                                update_interval=1)
     cache = m.MaskCache()
-    out, st = m.run_step(Q, K, V, dims, m.ScoringParams(b, bs), sched, cache, layer=0, step=0, check_finite=True)
+    out, st = m.run_step(Q, K, V, dims, m.ScoringParams(b, bs), sched, cache, layer=0, step=0)
     out = host(out.float())
     fwd = ora.hilbert3d_order(dims)
     inv = ora.invert_permutation(fwd)
