@@ -162,6 +162,11 @@ typedef struct {
    * the kernel (curve.cpp:166 apply_permutation without a permuted copy of Q);
    * k and v keep `in_layout`. */
   const uint32_t* in_rows;
+  /* ABI 2. Peer-scattered output (device pointer to a dfs_peer_table, or NULL): output
+   * row i (after out_rows) is raster token t = out_rows[i], written to rank
+   * t / n_local's [n_local, heads_total, dv] shard at row t % n_local, head
+   * h0 + h — the reverse Ulysses all-to-all fused into the epilogue (tcgen05 K5 only). */
+  const void* out_peers;
 } dfs_attn_args;
 int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream);
 
@@ -241,6 +246,60 @@ typedef struct {
   int64_t dv; /* head dim of v / o; 0 = d (dv != d: DFS_F32 with n <= DFS_COMPAT_MAX_ROWS only) */
 } dfs_step_args;
 int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
+
+/* ================ Ulysses: the all-to-all fused into K2 and K5 ================ */
+/* a DiT that keeps q/k/v/o sequence-sharded ([N/P, H, d] per rank,
+ * rank r holding raster tokens [r*N/P, (r+1)*N/P)) runs the step for its head
+ * group [r*H/P, (r+1)*H/P) straight on its peers' shards over NVLink: K2 pulls the
+ * token rows of its heads from every peer (P2P loads — the seq->head all-to-all
+ * and its unpack are the gather's addressing) and K5's epilogue stores every output
+ * row into the shard of the rank that owns the token (P2P stores — the head->seq
+ * all-to-all and its pack). No exchange pass, no pack/unpack copies, no NCCL call on
+ * the data path. Buffers are shared once per allocation with CUDA IPC. */
+#define DFS_MAX_PEERS 16
+typedef struct {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} dfs_peer_handle;
+/* IPC handle of a device allocation (cudaMalloc'd base pointer) for the other ranks. */
+int dfs_alltoall_export(const void* dev_ptr, dfs_peer_handle* out);
+/* Maps a peer's allocation into this process (peer access enabled lazily over NVLink). */
+int dfs_alltoall_import(const dfs_peer_handle* handle, void** dev_ptr);
+int dfs_alltoall_close(void* dev_ptr);
+/* Device-resident table of the ranks' shard pointers (what K2/K5 index by token). */
+typedef struct {
+  const void* ptr[DFS_MAX_PEERS];
+  int64_t n_local;     /* tokens per rank shard */
+  int64_t heads_total; /* H of the [n_local, H, d] shards */
+  int64_t h0;          /* first head of this rank's group */
+} dfs_peer_table;
+/* One Alg. 1 step (scheduler.cpp:91-135) for this rank's head group on
+ * sequence-sharded bf16 activations. q/k/v[r] and o[r]: rank r's [n_local, H, d] shard
+ * as mapped in THIS process (own shard = local pointer). Every rank calls it with the
+ * same step; callers synchronise the ranks (barrier) before the step — peers' inputs
+ * written — and after it — this rank's output rows written by the peers. Stats are
+ * per local head. */
+typedef struct {
+  const void* q[DFS_MAX_PEERS];
+  const void* k[DFS_MAX_PEERS];
+  const void* v[DFS_MAX_PEERS];
+  void* o[DFS_MAX_PEERS];
+  int world;
+  int rank;
+  int64_t n_local;
+  int64_t heads; /* H (all ranks); H % world == 0 */
+  int64_t d;
+  int64_t frames, height, width; /* token lattice, frames*height*width = world*n_local */
+  int64_t block;
+  int64_t sub_block;
+  int layer;
+  int step;
+  int force_dense;
+  int* dense_out;
+  double* budget_out;
+  int* updated_out;     /* [H / world] */
+  double* sparsity_out; /* [H / world] */
+} dfs_alltoall_step_args;
+int dfs_alltoall_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_alltoall_step_args* a, dfs_stream stream);
 
 /* ============ Matrix-level companions used by the dfs:: drop-in shim =========== */
 /* attention.cpp:105-123 attention_scores (and the pooled softmax inside

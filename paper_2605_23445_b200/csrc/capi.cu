@@ -882,7 +882,7 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     pk = h->pooled_k.as<float>();
   }
   // attention operands after the reorder
-  const void *att_q = a->q, *att_k = h->k_hnd.p, *att_v = h->v_hnd.p;
+  const void *att_q = a->q, *att_k = nullptr, *att_v = nullptr;
   if (compat) {
     // reorder q, k, v into fp32 [H, N, d] (pooled rows of q and k fused in)
     if ((rc = h->f32_q.ensure(sizeof(float) * size_t(n * H * d))) ||
@@ -905,6 +905,8 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     // re-read by every query block that selects them, so they get one permuted [H, N, d]
     // copy each (K with the pooled rows fused in).
     if ((rc = h->k_hnd.ensure(tok16)) || (rc = h->v_hnd.ensure(tok16))) return rc;
+    att_k = h->k_hnd.p;
+    att_v = h->v_hnd.p;
     const void *q = a->q, *k = a->k, *v = a->v;
     if (dtype == DFS_F32) {
       // pooled rows from the fp32 values (what dfs::build_mask scores), then bf16 copies

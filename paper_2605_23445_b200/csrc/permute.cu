@@ -51,13 +51,17 @@ __device__ __forceinline__ void unpack<__nv_bfloat16>(const uint4& u, float (&x)
 
 // One CTA = `rows` consecutive destination rows (a pooling group when pooling)
 // x all heads. Thread slots walk (head, 16B column chunk).
-template <typename T, bool kPool, bool kScatter>
+// kPeer: the source is sequence-sharded over the ranks (dfs_peer_table, Ulysses): token
+// si of head h lives in rank si / n_local's [n_local, H, d] shard, row si % n_local,
+// head h0 + h — read over NVLink from the peer's memory (plain loads: no .nc on peers).
+template <typename T, bool kPool, bool kScatter, bool kPeer = false>
 __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src, int src_layout,
                                                       T* __restrict__ dst, int dst_layout,
                                                       const uint32_t* __restrict__ idx, int64_t n,
                                                       int64_t heads, int64_t d, int rows,
                                                       float* __restrict__ pooled, int64_t pool,
-                                                      int32_t* __restrict__ nonfinite) {
+                                                      int32_t* __restrict__ nonfinite,
+                                                      const dfs_peer_table* __restrict__ peers = nullptr) {
   constexpr int V = Vec<T>::N;
   // independent 16-byte row loads in flight per thread: 4 keeps the pooling variant at
   // <= 56 registers (3 CTAs of 384 threads per SM); 8 or 16 cost more in occupancy than
@@ -76,6 +80,11 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
       si = kScatter ? i : int64_t(idx[i]);
       di = kScatter ? int64_t(idx[i]) : i;
       if (si >= n || di >= n) si = di = -1;  // invalid permutation entry: no wild access
+    }
+    if (kPeer && si >= 0) {  // absolute address of the row's head-group start in its owner's shard
+      const int64_t r = si / peers->n_local;
+      si = int64_t(reinterpret_cast<uintptr_t>(static_cast<const T*>(peers->ptr[r]) +
+                                               ((si - r * peers->n_local) * peers->heads_total + peers->h0) * d));
     }
     s_src[t] = si;
     s_dst[t] = di;
@@ -102,8 +111,12 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
 #pragma unroll
       for (int k = 0; k < kBatch; ++k) {
         const int64_t si = rb + k < rows ? s_src[rb + k] : -1;
-        u[k] = si >= 0 ? __ldg(reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c))
-                       : make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (kPeer)
+          u[k] = si >= 0 ? *reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(si) + h * d + c)
+                         : make_uint4(0u, 0u, 0u, 0u);
+        else
+          u[k] = si >= 0 ? __ldg(reinterpret_cast<const uint4*>(src + row_offset(src_layout, n, heads, d, h, si) + c))
+                         : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
       for (int k = 0; k < kBatch; ++k) {
@@ -254,6 +267,34 @@ __global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ src, floa
 }
 
 }  // namespace
+
+// K2 over sequence-sharded peers (Ulysses): gather + pool + finite check of this rank's
+// head group, bf16 only, destination [heads, n, d] (HND) or NULL (read-only pooling pass)
+int permute_rows_peer_impl(const dfs_peer_table* peers_dev, int64_t heads_total, void* dst, const uint32_t* idx,
+                           int64_t n, int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite,
+                           cudaStream_t stream) {
+  using T = __nv_bfloat16;
+  if (d % 8 || (pooled && pool > 64) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(DFS_E_UNSUPPORTED, "alltoall: d must be a multiple of 8 and pool <= 64");
+  const int64_t rows = pooled ? pool : 16;
+  const int64_t grid = ceil_div(n, rows);
+  const int64_t slots = heads * (d / 8);
+  const int64_t ysplit = ceil_div(slots, 384);
+  const int threads = int(ceil_div(ceil_div(slots, ysplit), 32) * 32);
+  if (grid > int64_t(INT32_MAX) || ysplit > 65535) return fail(DFS_E_UNSUPPORTED, "alltoall: too many rows");
+  (void)heads_total;
+  const dim3 g{unsigned(grid), unsigned(ysplit), 1u};
+  if (pooled)
+    permute_kernel<T, true, false, true><<<g, threads, 0, stream>>>(nullptr, DFS_NHD, static_cast<T*>(dst), DFS_HND,
+                                                                   idx, n, heads, d, int(rows), pooled, pool,
+                                                                   nonfinite, peers_dev);
+  else
+    permute_kernel<T, false, false, true><<<g, threads, 0, stream>>>(nullptr, DFS_NHD, static_cast<T*>(dst),
+                                                                    DFS_HND, idx, n, heads, d, int(rows), nullptr, 1,
+                                                                    nonfinite, peers_dev);
+  DFS_LAUNCH_CHECK("permute_rows_peer");
+  return DFS_OK;
+}
 
 int cast_impl(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t count, int32_t* nonfinite,
               cudaStream_t stream) {
