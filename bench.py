@@ -43,11 +43,11 @@ WORKLOADS = {  # SURVEY.md §8 config shorthand
 METRIC = "block-sparse attn effective TFLOPS (dense-equivalent) per call, HunyuanVideo 720p, 90% sparsity"
 
 
-def metric_for(workload: str) -> str:
+def metric_for(workload: str, wl: dict | None = None) -> str:
     """BASELINE.json's metric for the headline workload; the other configs name themselves."""
-    if workload == "HY":
+    w = wl or WORKLOADS[workload]
+    if workload == "HY" and w["gamma"] == WORKLOADS["HY"]["gamma"]:
         return METRIC
-    w = WORKLOADS[workload]
     return f"block-sparse attn effective TFLOPS (dense-equivalent) per call, {w['name']}"
 
 
@@ -282,7 +282,7 @@ def run_reference(args, wl):
     call_s, units_s, fixed_s, units = runs[len(runs) // 2]
     value = dense_flops / call_s / 1e12
     sample = rs.describe(call_s, units_s, fixed_s, units, reps=len(runs))
-    out = {"metric": metric_for(args.workload), "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+    out = {"metric": metric_for(args.workload, wl), "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": call_s * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic iid normal (content does not change CPU op count)",
            "config": {"workload": wl["name"], "tokens": n, "heads": H, "d": d, "block": B, "sub_block": Bs,
@@ -371,7 +371,7 @@ def run_trajectory_bench(args, wl, dfs, dev, world, rank, local, dist):
     if rank != 0:
         dist.destroy_process_group()
         return
-    res = {"metric": metric_for(args.workload) + " (averaged over a 50-step mask-caching trajectory)",
+    res = {"metric": metric_for(args.workload, wl) + " (averaged over a 50-step mask-caching trajectory)",
            "value": dense_flops_total / steps / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
            "steps": steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "bf16", "data": "synthetic smooth Gaussian video fields",
@@ -392,6 +392,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="HY", choices=sorted(WORKLOADS))
+    ap.add_argument("--gamma", type=float, default=None,
+                    help="override the workload's block budget (W7 sparsity sweep: 0.30 ... 0.05)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-units-per-thread", type=int, default=0,
                     help="reference arm sample size per step (0: sized for a ~2.5 min run)")
@@ -404,7 +406,10 @@ def main():
                     help="sequence-sharded inputs [N/P, H, d]: NCCL all-to-all to heads, step, all-to-all back "
                          "(inside the timed region); default: head-sharded inputs, no collective")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    if args.gamma is not None:
+        wl["gamma"] = args.gamma
+        wl["name"] = wl["name"].split(",")[0] + f", {round(100 * (1 - args.gamma))}% block sparsity (gamma={args.gamma})"
     if args.impl == "reference":
         run_reference(args, wl)
         return
@@ -542,6 +547,17 @@ def main():
                                        phase_fraction=1.0, update_interval=2)
     dfs.run_step(q, k, v, dims, params, sched_reuse, cache, layer=1, step=0, out=out)
     t_reuse = timed(lambda: dfs.run_step(q, k, v, dims, params, sched_reuse, cache, layer=1, step=1, out=out))
+    # K1 (token order): once per lattice geometry, cached by the handle, so outside the call
+    t_k1 = timed(lambda: dfs.hilbert3d_order(dims))
+    # LUT overlap of query-block pairs (2u, 2u+1): |I_u ∪ I_u+1| / K, and the
+    # fraction of query blocks that select their own (diagonal) block
+    pairs = lut[:, : (m // 2) * 2].reshape(hl, m // 2, 2 * K)
+    srt = pairs.sort(-1).values
+    union = 1 + (srt[..., 1:] != srt[..., :-1]).sum(-1)
+    diag = (lut == torch.arange(m, device=dev).view(1, m, 1)).any(-1).float().mean().item()
+    overlap = {"pair_union_over_K_mean": float(union.float().mean().item() / K),
+               "pair_union_over_K_min": float(union.min().item() / K),
+               "pair_union_over_K_max": float(union.max().item() / K), "diag_selected_frac": diag}
 
     exec_flops = executed_flops(lut, n, B, d)
     if world > 1:
@@ -629,7 +645,7 @@ def main():
     # reorder + fused unpermute)
     launches_per_step = 3 + 3 + 1 + 1 + 1
     res = {
-        "metric": metric_for(args.workload), "value": dense_flops / (ms_max * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
+        "metric": metric_for(args.workload, wl), "value": dense_flops / (ms_max * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic smooth Gaussian video fields (4 smoothing rounds), generated on device",
@@ -637,6 +653,8 @@ def main():
                    "sub_block": Bs, "gamma": gamma, "K": K, "M": m, "parallelism": (f"ulysses all-to-all x{world}" if ulysses_mode else f"head-shard x{world}"),
                    "l2": "inputs 3x730 MB bf16 > 126 MB L2 (no flush needed)"},
         "ms_per_call_mask_reuse": t_reuse,
+        "order_K1_ms_per_geometry": t_k1,
+        "lut_overlap": overlap,
         "executed_tflop_per_call": exec_flops / 1e12, "dense_equiv_tflop_per_call": dense_flops / 1e12,
         "executed_tflops": exec_flops / (ms_max * 1e-3) / 1e12,
         "breakdown_ms": {"reorder_pool_K2": t_perm, "score_K3": t_score, "topk_K4": t_topk,

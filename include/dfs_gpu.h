@@ -258,12 +258,15 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, d
  * the data path. Buffers are shared once per allocation with CUDA IPC. */
 #define DFS_MAX_PEERS 16
 typedef struct {
-  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t of the allocation that holds the buffer */
+  int64_t offset;          /* byte offset of the buffer inside that allocation */
 } dfs_peer_handle;
-/* IPC handle of a device allocation (cudaMalloc'd base pointer) for the other ranks. */
+/* IPC handle of any device buffer (e.g. a sub-allocation of a caching allocator). */
 int dfs_alltoall_export(const void* dev_ptr, dfs_peer_handle* out);
-/* Maps a peer's allocation into this process (peer access enabled lazily over NVLink). */
+/* Maps a peer's buffer into this process (peer access enabled lazily over NVLink); an
+ * allocation exported several times is mapped once and reference counted. */
 int dfs_alltoall_import(const dfs_peer_handle* handle, void** dev_ptr);
+/* Releases a pointer returned by dfs_alltoall_import. */
 int dfs_alltoall_close(void* dev_ptr);
 /* Device-resident table of the ranks' shard pointers (what K2/K5 index by token). */
 typedef struct {

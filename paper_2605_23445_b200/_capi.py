@@ -39,7 +39,23 @@ class AttnArgs(C.Structure):
     _fields_ = [("q", _p), ("k", _p), ("v", _p), ("o", _p), ("dtype", _i32), ("in_layout", _i32),
                 ("out_layout", _i32), ("heads", _i64), ("nq", _i64), ("nk", _i64), ("d", _i64),
                 ("block", _i64), ("blk_ptr", _p), ("blk_idx", _p), ("out_rows", _p), ("scale", _f),
-                ("force_generic", _i32), ("dv", _i64), ("in_rows", _p)]
+                ("force_generic", _i32), ("dv", _i64), ("in_rows", _p), ("out_peers", _p)]
+
+
+MAX_PEERS = 16
+
+
+class PeerHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64), ("offset", _i64)]
+
+
+class AlltoallStepArgs(C.Structure):
+    _fields_ = [("q", _p * MAX_PEERS), ("k", _p * MAX_PEERS), ("v", _p * MAX_PEERS), ("o", _p * MAX_PEERS),
+                ("world", _i32), ("rank", _i32), ("n_local", _i64), ("heads", _i64), ("d", _i64),
+                ("frames", _i64), ("height", _i64), ("width", _i64), ("block", _i64), ("sub_block", _i64),
+                ("layer", _i32), ("step", _i32), ("force_dense", _i32), ("dense_out", C.POINTER(_i32)),
+                ("budget_out", C.POINTER(_dbl)), ("updated_out", C.POINTER(_i32)),
+                ("sparsity_out", C.POINTER(_dbl))]
 
 
 class Schedule(C.Structure):
@@ -84,7 +100,11 @@ _SIGS = {
     "dfs_mask_cache_size": (_i32, [_p, C.POINTER(_i64)]),
     "dfs_mask_cache_info": (_i32, [_p, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32)]),
     "dfs_cast": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
+    "dfs_alltoall_export": (_i32, [_p, C.POINTER(PeerHandle)]),
+    "dfs_alltoall_import": (_i32, [C.POINTER(PeerHandle), C.POINTER(_p)]),
+    "dfs_alltoall_close": (_i32, [_p]),
     "dfs_run_step": (_i32, [_p, C.POINTER(Schedule), C.POINTER(StepArgs), _p]),
+    "dfs_alltoall_run_step": (_i32, [_p, C.POINTER(Schedule), C.POINTER(AlltoallStepArgs), _p]),
     "dfs_softmax_scores": (_i32, [_p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _dbl, _p, _p]),
     "dfs_aggregate_scores": (_i32, [_p, _i64, _i64, _i64, _i64, _p, _p]),
     "dfs_top_indices": (_i32, [_p, _i64, _i64, _i64, _p, _p]),

@@ -86,6 +86,7 @@ struct Params {
   const uint32_t* in_rows;  // fused Q reorder: logical query row i = raster token in_rows[i] (NULL: tiles)
   unsigned long long* trace;  // debug timeline (DFS_ATTN_TRACE), NULL in production
   int64_t tiles;
+  const dfs_peer_table* out_peers;  // Ulysses: rows go to the token owner's shard (NULL: p.out)
 };
 
 struct Bars {
@@ -521,7 +522,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kOC; ++c) ov[c] = 0u;
       }
       if (i < p.nq) {
-        __nv_bfloat16* dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
+        __nv_bfloat16* dst;
+        if (p.out_peers) {  // the reverse all-to-all: P2P store into the owning rank's [n_local, H, d] shard
+          const int64_t nl = p.out_peers->n_local, r = orow / nl;
+          dst = static_cast<__nv_bfloat16*>(const_cast<void*>(p.out_peers->ptr[r])) +
+                ((orow - r * nl) * p.out_peers->heads_total + p.out_peers->h0 + h) * D + wg * kOC;
+        } else {
+          dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
+        }
 #pragma unroll
         // 32-byte stores (STG.256): half the store instructions of 16-byte ones; the store
         // issue at the tile boundary is what holds the warps there
@@ -659,7 +667,8 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   p.out_rows = a.out_rows;
   p.out = static_cast<__nv_bfloat16*>(a.o);
   p.out_layout = a.out_layout;
-  p.out_v8 = (reinterpret_cast<uintptr_t>(a.o) & 31) == 0;
+  p.out_peers = static_cast<const dfs_peer_table*>(a.out_peers);
+  p.out_v8 = !a.out_peers && (reinterpret_cast<uintptr_t>(a.o) & 31) == 0;  // peer shards: 16-byte stores
   p.in_nhd = a.in_layout == DFS_NHD;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.in_rows = a.in_rows;

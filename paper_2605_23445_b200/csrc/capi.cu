@@ -10,8 +10,11 @@
 //   run_step          scheduler.cpp:91-135 (dense steps skip the reorder)
 // The per-head loop of the reference becomes one batched launch per kernel over
 // all H heads of the layer; the unpermute is fused into the attention epilogue.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -35,6 +38,9 @@ int permute_rows_impl(const void* src, int src_layout, void* dst, int dst_layout
 int finite_check_impl(const void* x, int64_t count, int dtype, int32_t* flag, cudaStream_t stream);
 int cast_impl(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t count, int32_t* nonfinite,
               cudaStream_t stream);
+int permute_rows_peer_impl(const dfs_peer_table* peers_dev, int64_t heads_total, void* dst, const uint32_t* idx,
+                           int64_t n, int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite,
+                           cudaStream_t stream);
 int score_blocks_generic(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
                          int64_t sub_block, double* S, float* P_ws, int64_t P_ws_floats, cudaStream_t stream);
 int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
@@ -147,11 +153,12 @@ struct dfs_handle {
   Buf step_flag;                         // the step's non-finite flag (dfs_step_args.nonfinite == NULL)
   Buf q16, k16, v16, o16;                // DFS_F32 steps past the compatibility cap: bf16 copies
   Buf f32_q, f32_k, f32_v, probs, bits;  // DFS_F32 compatibility steps: reordered fp32 [H, N, d]
+  Buf peer_tabs;                         // Ulysses: q/k/v/o dfs_peer_table on the device
   int64_t total_bytes() const {
     int64_t t = 0;
     for (const Buf* b : {&scratch_i32, &flag, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
                          &lut, &sel, &counts, &tmp_ptr, &tmp_idx, &recall_ws, &step_flag, &q16, &k16, &v16,
-                         &o16, &f32_q, &f32_k, &f32_v, &probs, &bits})
+                         &o16, &f32_q, &f32_k, &f32_v, &probs, &bits, &peer_tabs})
       t += int64_t(b->bytes);
     return t;
   }
@@ -217,6 +224,8 @@ float resolve_scale(float scale, int64_t d) { return scale > 0.f ? scale : float
 
 int attn_dispatch(dfs_handle* h, const dfs_attn_args& a, cudaStream_t stream) {
   const float scale = resolve_scale(a.scale, a.d);
+  if (a.out_peers && (a.force_generic || h->opt_generic_attn || !attn_sm100_supports(a)))
+    return fail(DFS_E_UNSUPPORTED, "sparse_attn: peer-scattered output needs the tcgen05 kernel");
   if (!a.force_generic && !h->opt_generic_attn && attn_sm100_supports(a)) return sparse_attn_sm100(a, scale, stream);
   return sparse_attn_generic(a, scale, stream);
 }
@@ -331,6 +340,7 @@ int dfs_validate_permutation(dfs_handle* h, const uint32_t* fwd, int64_t n, int*
 int dfs_permute_rows(const void* src, int src_layout, void* dst, int dst_layout, int dtype, const uint32_t* idx,
                      int64_t n, int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite,
                      dfs_stream stream) {
+  NvtxRange nvtx("dfs_permute_rows");
   if (!src || !idx || (!dst && !pooled && !nonfinite)) return fail(DFS_E_INVALID, "permute_rows: null pointer");
   return permute_rows_impl(src, src_layout, dst, dst_layout, dtype, idx, n, heads, d, pooled, pool, nonfinite,
                            false, as_stream(stream));
@@ -346,6 +356,7 @@ int dfs_unpermute_rows(const void* src, int src_layout, void* dst, int dst_layou
 // ------------------------------------------------------------- K3 / K4 -----
 int dfs_score_blocks(dfs_handle* h, const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d,
                      int64_t block, int64_t sub_block, double* scores, dfs_stream stream) {
+  NvtxRange nvtx("dfs_score_blocks");
   if (int rc = check_handle(h)) return rc;
   if (sub_block < 1 || block < sub_block)
     return fail(DFS_E_INVALID, "ScoringParams: need 1 <= sub_block_size <= block_size");
@@ -366,6 +377,7 @@ int dfs_topk_count(double budget, int64_t m, int64_t* k) {
 
 int dfs_topk_select(const double* scores, int64_t heads, int64_t m, int64_t k, int32_t* lut, uint8_t* bits,
                     dfs_stream stream) {
+  NvtxRange nvtx("dfs_topk_select");
   if (!scores || m < 1 || heads < 1) return fail(DFS_E_INVALID, "topk_select: scores must be square and non-empty");
   uint8_t* sel = nullptr;
   cudaStream_t s = as_stream(stream);
@@ -389,6 +401,7 @@ int dfs_lut_row_ptr(int64_t heads, int64_t m, int64_t k, int32_t* blk_ptr, dfs_s
 
 // ---------------------------------------------------------------- K5 -------
 int dfs_sparse_attn_fwd(dfs_handle* h, const dfs_attn_args* a, dfs_stream stream) {
+  NvtxRange nvtx("dfs_sparse_attn_fwd");
   if (int rc = check_handle(h)) return rc;
   if (!a || !a->q || !a->k || !a->v || !a->o) return fail(DFS_E_INVALID, "sparse_attn: null pointer");
   if (a->nq < 1 || a->nk < 1 || a->d < 1 || a->heads < 1)
@@ -645,6 +658,7 @@ int dfs_mask_cache_get(dfs_handle* h, int layer, int head, uint8_t* bits, int* l
 int dfs_block_recall(dfs_handle* h, const void* q, const void* k, int layout, const uint32_t* q_rows, int64_t heads,
                      int64_t n, int64_t d, const int32_t* blk_ptr, const int32_t* blk_idx, double* recall_host,
                      dfs_stream stream) {
+  NvtxRange nvtx("dfs_block_recall");
   if (int rc = check_handle(h)) return rc;
   if (!q || !k || !blk_ptr || !blk_idx || !recall_host || heads < 1 || n < 1)
     return fail(DFS_E_INVALID, "block_recall: bad arguments");
@@ -743,6 +757,74 @@ int compat_scores(dfs_handle* h, const float* pq, const float* pk, int64_t H, in
   return DFS_OK;
 }
 
+// Scoring (K3, or the compatibility scorer), top-K (K4) and the commit of the new masks
+// of heads `need` into the layer's device CSR (scheduler.cpp:113-116 build_mask +
+// cache.store). Runs only after the step's non-finite check passed.
+int build_and_commit(dfs_handle* h, int layer, int step, const std::vector<int>& need, int64_t H, int64_t m,
+                     int64_t n, int64_t d, int64_t B, int64_t Bs, double budget, bool compat, const float* pq,
+                     const float* pk, LayerMasks** Lout, cudaStream_t s) {
+  int rc;
+  int64_t K;
+  if ((rc = dfs_topk_count(budget, m, &K))) return rc;
+  if ((rc = h->scores.ensure(sizeof(double) * size_t(H * m * m)))) return rc;
+  if (compat)
+    rc = compat_scores(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
+  else
+    rc = score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
+  if (rc) return rc;
+  if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large");
+  if (int64_t(need.size()) == H) {
+    // common case: every head refreshes -> the LUT becomes the layer's CSR in place
+    LayerMasks& NL = h->masks[layer];
+    NL.heads = H;
+    NL.m = m;
+    NL.block = B;
+    NL.head.assign(size_t(H), HeadMask{});
+    NL.head_off.resize(size_t(H));
+    if ((rc = NL.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))) ||
+        (rc = NL.idx.ensure(sizeof(int32_t) * size_t(H * m * K))))
+      return rc;
+    if ((rc = topk_select_impl(h->scores.as<double>(), H, m, K, NL.idx.as<int32_t>(), nullptr, nullptr, s)))
+      return rc;
+    if ((rc = lut_row_ptr_impl(H, m, K, NL.ptr.as<int32_t>(), s))) return rc;
+    for (int64_t hh = 0; hh < H; ++hh) {
+      NL.head[size_t(hh)] = HeadMask{true, step, m * K};
+      NL.head_off[size_t(hh)] = hh * m * K;
+    }
+    *Lout = &NL;
+    return DFS_OK;
+  }
+  if ((rc = h->lut.ensure(sizeof(int32_t) * size_t(H * m * K))) ||
+      (rc = h->tmp_ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))))
+    return rc;
+  if ((rc = topk_select_impl(h->scores.as<double>(), H, m, K, h->lut.as<int32_t>(), nullptr, nullptr, s))) return rc;
+  if ((rc = lut_row_ptr_impl(1, m, K, h->tmp_ptr.as<int32_t>(), s))) return rc;
+  LayerMasks& NL = h->masks[layer];
+  if (NL.m == 0) {
+    NL.heads = H;
+    NL.m = m;
+    NL.block = B;
+    NL.head.assign(size_t(H), HeadMask{});
+    NL.head_off.assign(size_t(H), 0);
+    if ((rc = NL.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1)))) return rc;
+    DFS_CUDA_CHECK(cudaMemsetAsync(NL.ptr.p, 0, sizeof(int32_t) * size_t(H * m + 1), s));
+  }
+  std::vector<const int32_t*> ps, is;
+  std::vector<int64_t> ns;
+  for (int hh : need) {
+    ps.push_back(h->tmp_ptr.as<int32_t>());
+    is.push_back(h->lut.as<int32_t>() + int64_t(hh) * m * K);
+    ns.push_back(m * K);
+  }
+  if ((rc = layer_replace_heads(h, NL, need, ps, is, ns, s))) return rc;
+  for (int hh : need) {
+    NL.head[size_t(hh)].valid = true;
+    NL.head[size_t(hh)].last_update_step = step;
+  }
+  *Lout = &NL;
+  return DFS_OK;
+}
+
 int attn_simple(dfs_handle* h, const void* q, const void* k, const void* v, void* o, int dtype, int in_layout,
                 const uint32_t* in_rows, int out_layout, const uint32_t* out_rows, int64_t H, int64_t n, int64_t d,
                 int64_t dv, int64_t B, const int32_t* blk_ptr, const int32_t* blk_idx, cudaStream_t s) {
@@ -781,6 +863,7 @@ extern "C" {
 //   fp32, n > cap   pooling and scoring from the fp32 values (tcgen05 fp16x3 = fp32
 //                   accurate), inputs rounded to bf16 for K5, output converted back.
 int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* a, dfs_stream stream) {
+  NvtxRange nvtx("dfs_run_step");
   if (int rc = check_handle(h)) return rc;
   if (!a || !a->q || !a->k || !a->v || !a->o) return fail(DFS_E_INVALID, "run_step: null pointer");
   cudaStream_t s = as_stream(stream);
@@ -934,69 +1017,9 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   }
   if ((rc = check_flag(flag, s))) return rc;  // nothing scored, cached or written yet
 
-  if (update_any) {
-    int64_t K;
-    if ((rc = dfs_topk_count(budget, m, &K))) return rc;
-    if ((rc = h->scores.ensure(sizeof(double) * size_t(H * m * m)))) return rc;
-    pq = h->pooled_q.as<float>();
-    pk = h->pooled_k.as<float>();
-    if (compat)
-      rc = compat_scores(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
-    else
-      rc = score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
-    if (rc) return rc;
-    if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large");
-    if (int(need.size()) == H) {
-      // common case: every head refreshes -> the LUT becomes the layer's CSR in place
-      LayerMasks& NL = h->masks[a->layer];
-      NL.heads = H;
-      NL.m = m;
-      NL.block = B;
-      NL.head.assign(size_t(H), HeadMask{});
-      NL.head_off.resize(size_t(H));
-      if ((rc = NL.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))) ||
-          (rc = NL.idx.ensure(sizeof(int32_t) * size_t(H * m * K))))
-        return rc;
-      if ((rc = topk_select_impl(h->scores.as<double>(), H, m, K, NL.idx.as<int32_t>(), nullptr, nullptr, s)))
-        return rc;
-      if ((rc = lut_row_ptr_impl(H, m, K, NL.ptr.as<int32_t>(), s))) return rc;
-      for (int64_t hh = 0; hh < H; ++hh) {
-        NL.head[size_t(hh)] = HeadMask{true, a->step, m * K};
-        NL.head_off[size_t(hh)] = hh * m * K;
-      }
-      L = &NL;
-    } else {
-      if ((rc = h->lut.ensure(sizeof(int32_t) * size_t(H * m * K))) ||
-          (rc = h->tmp_ptr.ensure(sizeof(int32_t) * size_t(H * m + 1))))
-        return rc;
-      if ((rc = topk_select_impl(h->scores.as<double>(), H, m, K, h->lut.as<int32_t>(), nullptr, nullptr, s)))
-        return rc;
-      if ((rc = lut_row_ptr_impl(1, m, K, h->tmp_ptr.as<int32_t>(), s))) return rc;
-      LayerMasks& NL = h->masks[a->layer];
-      if (NL.m == 0) {
-        NL.heads = H;
-        NL.m = m;
-        NL.block = B;
-        NL.head.assign(size_t(H), HeadMask{});
-        NL.head_off.assign(size_t(H), 0);
-        if ((rc = NL.ptr.ensure(sizeof(int32_t) * size_t(H * m + 1)))) return rc;
-        DFS_CUDA_CHECK(cudaMemsetAsync(NL.ptr.p, 0, sizeof(int32_t) * size_t(H * m + 1), s));
-      }
-      std::vector<const int32_t*> ps, is;
-      std::vector<int64_t> ns;
-      for (int hh : need) {
-        ps.push_back(h->tmp_ptr.as<int32_t>());
-        is.push_back(h->lut.as<int32_t>() + int64_t(hh) * m * K);
-        ns.push_back(m * K);
-      }
-      if ((rc = layer_replace_heads(h, NL, need, ps, is, ns, s))) return rc;
-      for (int hh : need) {
-        NL.head[size_t(hh)].valid = true;
-        NL.head[size_t(hh)].last_update_step = a->step;
-      }
-      L = &NL;
-    }
-  }
+  if (update_any && (rc = build_and_commit(h, a->layer, a->step, need, H, m, n, d, B, Bs, budget, compat,
+                                             h->pooled_q.as<float>(), h->pooled_k.as<float>(), &L, s)))
+    return rc;
 
   // attention over the selected blocks; output row i -> raster row fwd[i] (scheduler.cpp:134)
   if (compat) {
@@ -1027,6 +1050,210 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     const bool upd = std::find(need.begin(), need.end(), int(hh)) != need.end();
     if (a->updated_out) a->updated_out[hh] = upd;
     if (a->sparsity_out) a->sparsity_out[hh] = 1.0 - double(L->head[size_t(hh)].nnz) / (double(m) * double(m));
+  }
+  return DFS_OK;
+}
+
+// ------------------------------------------------------------ Ulysses ------
+}  // extern "C"
+
+namespace capi_detail {
+// cuMemGetAddressRange through the runtime's driver entry point (the library does not
+// link libcuda directly, so it loads on machines without a driver: the CPU test suite)
+int mem_range(const void* p, CUdeviceptr* base, size_t* size) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(DFS_E_CUDA, "cuMemGetAddressRange unavailable");
+    fn = reinterpret_cast<Fn>(ptr);
+  }
+  if (fn(base, size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+    return fail(DFS_E_INVALID, "alltoall: not a device allocation");
+  return DFS_OK;
+}
+}  // namespace capi_detail
+
+extern "C" {
+
+int dfs_alltoall_export(const void* dev_ptr, dfs_peer_handle* out) {
+  static_assert(sizeof(out->bytes) == sizeof(cudaIpcMemHandle_t), "IPC handle size");
+  if (!dev_ptr || !out) return fail(DFS_E_INVALID, "alltoall_export: null argument");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (int rc = mem_range(dev_ptr, &base, &size)) return rc;
+  cudaIpcMemHandle_t hd;
+  DFS_CUDA_CHECK(cudaIpcGetMemHandle(&hd, reinterpret_cast<void*>(base)));
+  std::memcpy(out->bytes, &hd, sizeof(hd));
+  out->offset = int64_t(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return DFS_OK;
+}
+
+namespace {
+struct Mapped {
+  void* base;
+  int refs;
+};
+std::mutex g_ipc_mu;
+std::map<std::string, Mapped> g_ipc;  // handle bytes -> mapping
+}  // namespace
+
+int dfs_alltoall_import(const dfs_peer_handle* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(DFS_E_INVALID, "alltoall_import: null argument");
+  std::lock_guard<std::mutex> g(g_ipc_mu);
+  const std::string key(reinterpret_cast<const char*>(handle->bytes), sizeof(handle->bytes));
+  auto it = g_ipc.find(key);
+  if (it == g_ipc.end()) {
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle->bytes, sizeof(hd));
+    void* base = nullptr;
+    DFS_CUDA_CHECK(cudaIpcOpenMemHandle(&base, hd, cudaIpcMemLazyEnablePeerAccess));
+    it = g_ipc.emplace(key, Mapped{base, 0}).first;
+  }
+  ++it->second.refs;
+  *dev_ptr = static_cast<char*>(it->second.base) + handle->offset;
+  return DFS_OK;
+}
+
+int dfs_alltoall_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(DFS_E_INVALID, "alltoall_close: null pointer");
+  std::lock_guard<std::mutex> g(g_ipc_mu);
+  for (auto it = g_ipc.begin(); it != g_ipc.end(); ++it) {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (mem_range(it->second.base, &base, &size)) continue;
+    const auto p = reinterpret_cast<CUdeviceptr>(dev_ptr);
+    if (p < base || p >= base + size) continue;
+    if (--it->second.refs == 0) {
+      cudaIpcCloseMemHandle(it->second.base);
+      g_ipc.erase(it);
+    }
+    return DFS_OK;
+  }
+  return fail(DFS_E_INVALID, "alltoall_close: pointer was not imported");
+}
+
+// scheduler.cpp:91-135 for the rank's head group on sequence-sharded activations: the
+// seq->head all-to-all is K2's P2P gather, the head->seq all-to-all K5's P2P epilogue.
+int dfs_alltoall_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_alltoall_step_args* a,
+                          dfs_stream stream) {
+  NvtxRange nvtx("dfs_alltoall_run_step");
+  if (int rc = check_handle(h)) return rc;
+  if (!a) return fail(DFS_E_INVALID, "alltoall_run_step: null arguments");
+  const int P = a->world;
+  if (P < 1 || P > DFS_MAX_PEERS || a->rank < 0 || a->rank >= P)
+    return fail(DFS_E_INVALID, "alltoall_run_step: world must be 1..16 and 0 <= rank < world");
+  if (a->heads < 1 || a->heads % P) return fail(DFS_E_INVALID, "alltoall_run_step: heads must split over the ranks");
+  const int64_t nl = a->n_local, n = nl * P, Ht = a->heads, Hl = Ht / P, d = a->d, B = a->block, Bs = a->sub_block;
+  if (nl < 1 || a->frames * a->height * a->width != n)
+    return fail(DFS_E_INVALID, "alltoall_run_step: world * n_local must equal the lattice's token count");
+  for (int r = 0; r < P; ++r)
+    if (!a->q[r] || !a->k[r] || !a->v[r] || !a->o[r]) return fail(DFS_E_INVALID, "alltoall_run_step: null shard");
+  if (Bs < 1 || B < Bs || B % Bs) return fail(DFS_E_INVALID, "ScoringParams: sub_block_size must divide block_size");
+  if (B != 128 || (d != 64 && d != 128))
+    return fail(DFS_E_UNSUPPORTED, "alltoall_run_step: the fused exchange runs on the tcgen05 kernels (B = 128, d = 64|128)");
+  cudaStream_t s = as_stream(stream);
+  double budget;
+  int rc;
+  if ((rc = dfs_schedule_budget_at(sched, a->step, &budget))) return rc;
+  const int64_t m = ceil_div(n, B);
+  const int64_t h0 = int64_t(a->rank) * Hl;
+
+  // peer tables: q, k, v, o (device, read by K2 and K5's epilogue)
+  dfs_peer_table tab[4] = {};
+  for (int t = 0; t < 4; ++t) {
+    tab[t].n_local = nl;
+    tab[t].heads_total = Ht;
+    tab[t].h0 = h0;
+  }
+  for (int r = 0; r < P; ++r) {
+    tab[0].ptr[r] = a->q[r];
+    tab[1].ptr[r] = a->k[r];
+    tab[2].ptr[r] = a->v[r];
+    tab[3].ptr[r] = a->o[r];
+  }
+  if ((rc = h->peer_tabs.ensure(sizeof(tab)))) return rc;
+  DFS_CUDA_CHECK(cudaMemcpyAsync(h->peer_tabs.p, tab, sizeof(tab), cudaMemcpyHostToDevice, s));
+  DFS_CUDA_CHECK(cudaStreamSynchronize(s));  // tab is on the host stack
+  const dfs_peer_table* dtab = h->peer_tabs.as<dfs_peer_table>();
+
+  if ((rc = h->step_flag.ensure(sizeof(int32_t)))) return rc;
+  int32_t* flag = h->step_flag.as<int32_t>();
+  DFS_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+  const size_t tok16 = sizeof(__nv_bfloat16) * size_t(n * Hl * d);
+  if ((rc = h->q16.ensure(tok16)) || (rc = h->k_hnd.ensure(tok16)) || (rc = h->v_hnd.ensure(tok16))) return rc;
+
+  const bool dense = budget < 0.0 || a->force_dense;
+  const PermEntry* pe;
+  // dense steps run in raster order (scheduler.cpp:99-105): the identity gather
+  if ((rc = get_perm(h, dense ? DFS_RASTER : DFS_HILBERT3D, dense ? n : a->frames, dense ? 1 : a->height,
+                     dense ? 1 : a->width, s, &pe)))
+    return rc;
+  const uint32_t* fwd = pe->fwd.as<uint32_t>();
+
+  std::vector<int> need;
+  LayerMasks* L = nullptr;
+  if (!dense) {
+    int is_upd = 0;
+    dfs_schedule_is_update_step(sched, a->step, &is_upd);
+    auto it = h->masks.find(a->layer);
+    if (it != h->masks.end()) {
+      if (it->second.m != m || it->second.block != B || it->second.heads != Hl)
+        h->masks.erase(it);
+      else
+        L = &it->second;
+    }
+    for (int64_t hh = 0; hh < Hl; ++hh)
+      if (is_upd || !L || !L->head[size_t(hh)].valid) need.push_back(int(hh));
+  }
+  const bool update_any = !need.empty();
+  const int64_t pv = ceil_div(n, Bs);
+  if (update_any && ((rc = h->pooled_q.ensure(sizeof(float) * size_t(Hl * pv * d))) ||
+                     (rc = h->pooled_k.ensure(sizeof(float) * size_t(Hl * pv * d)))))
+    return rc;
+  float* pq = update_any ? h->pooled_q.as<float>() : nullptr;
+  float* pk = update_any ? h->pooled_k.as<float>() : nullptr;
+  // K2 over the peers: this rank's heads of every token, reordered, pooled, finite-checked
+  if ((rc = permute_rows_peer_impl(dtab + 0, Ht, h->q16.p, fwd, n, Hl, d, pq, pq ? Bs : 1, flag, s)) ||
+      (rc = permute_rows_peer_impl(dtab + 1, Ht, h->k_hnd.p, fwd, n, Hl, d, pk, pk ? Bs : 1, flag, s)) ||
+      (rc = permute_rows_peer_impl(dtab + 2, Ht, h->v_hnd.p, fwd, n, Hl, d, nullptr, 1, flag, s)))
+    return rc;
+  if ((rc = check_flag(flag, s))) return rc;
+  if (update_any &&
+      (rc = build_and_commit(h, a->layer, a->step, need, Hl, m, n, d, B, Bs, budget, false, pq, pk, &L, s)))
+    return rc;
+
+  dfs_attn_args at{};
+  at.q = h->q16.p;
+  at.k = h->k_hnd.p;
+  at.v = h->v_hnd.p;
+  at.o = a->o[a->rank];
+  at.dtype = DFS_BF16;
+  at.in_layout = DFS_HND;
+  at.out_layout = DFS_NHD;
+  at.heads = Hl;
+  at.nq = n;
+  at.nk = n;
+  at.d = d;
+  at.block = B;
+  at.blk_ptr = dense ? nullptr : L->ptr.as<int32_t>();
+  at.blk_idx = dense ? nullptr : L->idx.as<int32_t>();
+  at.out_rows = dense ? nullptr : fwd;
+  at.out_peers = dtab + 3;
+  if (!attn_sm100_supports(at) || h->opt_generic_attn)
+    return fail(DFS_E_UNSUPPORTED, "alltoall_run_step: shards must be 16-byte aligned for the tcgen05 kernel");
+  if ((rc = sparse_attn_sm100(at, resolve_scale(0.f, d), s))) return rc;
+
+  if (a->dense_out) *a->dense_out = dense;
+  if (a->budget_out) *a->budget_out = dense ? 1.0 : budget;
+  for (int64_t hh = 0; hh < Hl; ++hh) {
+    const bool upd = std::find(need.begin(), need.end(), int(hh)) != need.end();
+    if (a->updated_out) a->updated_out[hh] = upd;
+    if (a->sparsity_out)
+      a->sparsity_out[hh] = dense ? 0.0 : 1.0 - double(L->head[size_t(hh)].nnz) / (double(m) * double(m));
   }
   return DFS_OK;
 }

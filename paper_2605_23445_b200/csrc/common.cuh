@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <string>
 
 #include "dfs_gpu.h"
@@ -29,6 +31,16 @@ int cuda_fail(cudaError_t e, const char* where);
   } while (0)
 
 inline cudaStream_t as_stream(dfs_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// NVTX range over a C-ABI entry point (header-only NVTX3: free unless a profiler
+// such as nsys / ncu --nvtx is attached); names the stage in timelines and lets
+// ncu filter launches by range (--nvtx-include "dfs_run_step/").
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kNumSMs = 148;
 

@@ -92,3 +92,114 @@ def ulysses_run_step(q_local, k_local, v_local, dims, params, schedule, cache, l
 
     o = ulysses_attention(q_local, k_local, v_local, step_fn, group)
     return o, stats_box["stats"]
+
+
+# --------------------------------------------------------------------------- #
+# the all-to-all fused into K2 / K5 over peer memory (dfs_alltoall_*)          #
+# --------------------------------------------------------------------------- #
+
+
+def alltoall_step_local(shards, dims, params, schedule, cache, layer: int, step: int, rank: int,
+                        force_dense: bool = False):
+    """dfs_alltoall_run_step for `rank` given every rank's shard pointers as seen by this process.
+
+    shards: dict with lists "q", "k", "v", "o" of per-rank [N/P, H, d] bf16 CUDA tensors or raw
+    device pointers (ints). The rank's head group [rank*H/P, (rank+1)*H/P) is computed: K2 pulls its
+    heads' token rows from every shard, K5 stores each output row into the shard owning the token.
+    Returns StepStats for the rank's heads. Callers synchronise the ranks around the call."""
+    import ctypes as C
+
+    from . import _capi as capi
+    from .ops import StepStats, _dims, _stream
+
+    world = len(shards["q"])
+    if world > capi.MAX_PEERS:
+        raise ValueError(f"ulysses: at most {capi.MAX_PEERS} ranks")
+    ref = shards["q"][rank]
+    nl, h, d = ref.shape
+    if h % world:
+        raise ValueError(f"ulysses: {h} heads do not split over {world} ranks")
+    for key in ("q", "k", "v", "o"):
+        for t in shards[key]:
+            if isinstance(t, torch.Tensor) and (t.shape != ref.shape or t.dtype != torch.bfloat16 or
+                                                not t.is_contiguous()):
+                raise ValueError("ulysses: shards must be contiguous bf16 [N/P, H, d] tensors of one shape")
+    dims = _dims(dims)
+    hl = h // world
+
+    def ptrs(key):
+        arr = (C.c_void_p * capi.MAX_PEERS)()
+        for r, t in enumerate(shards[key]):
+            arr[r] = t.data_ptr() if isinstance(t, torch.Tensor) else int(t)
+        return arr
+
+    dense, budget = C.c_int(), C.c_double()
+    upd = (C.c_int * hl)()
+    spars = (C.c_double * hl)()
+    a = capi.AlltoallStepArgs(ptrs("q"), ptrs("k"), ptrs("v"), ptrs("o"), world, rank, nl, h, d, dims.frames,
+                              dims.height, dims.width, params.block_size, params.sub_block_size, layer, step,
+                              int(force_dense), C.pointer(dense), C.pointer(budget),
+                              C.cast(upd, C.POINTER(C.c_int)), C.cast(spars, C.POINTER(C.c_double)))
+    with cache.lock:
+        capi.call("dfs_alltoall_run_step", cache.handle.ptr, C.byref(schedule._s), C.byref(a), _stream())
+    return StepStats(bool(dense.value), budget.value, [bool(x) for x in upd], list(spars))
+
+
+class PeerExchange:
+    """One rank's view of every rank's sequence shards, mapped with CUDA IPC (dfs_alltoall_export /
+    import): the data path of fused_run_step never goes through NCCL or a staging copy.
+
+    q, k, v, o: this rank's [N/P, H, d] bf16 CUDA shards (o is written by the ranks' K5s)."""
+
+    def __init__(self, q, k, v, o, group=None):
+        import ctypes as C
+
+        from . import _capi as capi
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.local = {"q": q, "k": k, "v": v, "o": o}
+        mine = {}
+        for key, t in self.local.items():
+            hd = capi.PeerHandle()
+            capi.call("dfs_alltoall_export", C.c_void_p(t.data_ptr()), C.byref(hd))
+            mine[key] = (bytes(hd.bytes), int(hd.offset))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine, group=group)
+        self.shards = {key: [] for key in self.local}
+        self._opened = []
+        for r in range(self.world):
+            for key in self.local:
+                if r == self.rank:
+                    self.shards[key].append(self.local[key])
+                    continue
+                raw, off = everyone[r][key]
+                hd = capi.PeerHandle()
+                C.memmove(hd.bytes, raw, 64)
+                hd.offset = off
+                p = C.c_void_p()
+                capi.call("dfs_alltoall_import", C.byref(hd), C.byref(p))
+                self._opened.append(p.value)
+                self.shards[key].append(p.value)
+
+    def close(self):
+        import ctypes as C
+
+        from . import _capi as capi
+
+        for p in self._opened:
+            capi.call("dfs_alltoall_close", C.c_void_p(p))
+        self._opened = []
+
+    def fused_run_step(self, dims, params, schedule, cache, layer: int, step: int, force_dense: bool = False):
+        """Alg. 1 step on the sequence-sharded activations: every rank's K2 reads its heads from
+        all shards, every rank's K5 writes its heads' rows into all shards; barriers on both
+        sides make the peers' inputs and outputs visible. Returns the rank's head-group stats."""
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+        stats = alltoall_step_local(self.shards, dims, params, schedule, cache, layer, step, self.rank,
+                                    force_dense)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+        return stats
