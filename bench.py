@@ -402,6 +402,9 @@ def main():
                     help="diffusion trajectory: T=50 steps, 25%% dense warmup, phase budgets, mask update every "
                          "Delta=12 sparse steps (the device mask cache serves the other steps); reports per-step "
                          "averages over the whole schedule instead of the update-step call")
+    ap.add_argument("--ulysses-nccl", action="store_true",
+                    help="with --ulysses: exchange with torch.distributed NCCL all_to_all + pack/unpack copies "
+                         "instead of the exchange fused into K2/K5 over peer memory (dfs_alltoall_run_step)")
     ap.add_argument("--ulysses", action="store_true",
                     help="sequence-sharded inputs [N/P, H, d]: NCCL all-to-all to heads, step, all-to-all back "
                          "(inside the timed region); default: head-sharded inputs, no collective")
@@ -467,6 +470,8 @@ def main():
         ql, kl, vl = (x[rank * nl:(rank + 1) * nl].contiguous() for x in full)
         del full
         q, k, v = ulysses.seq_to_head([ql, kl, vl])  # head-local view, for the kernel breakdown only
+        ol = torch.empty_like(ql)
+        exch = None if args.ulysses_nccl else ulysses.PeerExchange(ql, kl, vl, ol)
     else:
         q, k, v = smooth_fields(dims, hl, d, seed=1000 + rank, device=dev)
     params = dfs.ScoringParams(B, Bs)
@@ -483,7 +488,9 @@ def main():
         torch.cuda.synchronize()
 
     def step():
-        if ulysses_mode:
+        if ulysses_mode and exch is not None:
+            exch.fused_run_step(dims, params, sched, cache, layer=0, step=0)
+        elif ulysses_mode:
             ulysses.ulysses_run_step(ql, kl, vl, dims, params, sched, cache, layer=0, step=0)
         else:
             dfs.run_step(q, k, v, dims, params, sched, cache, layer=0, step=0, out=out)
@@ -594,7 +601,12 @@ def main():
         stream.wait_event(ev_in[b])
         stream.wait_event(ev_out[b])  # step i-2's output has left the device buffer
         qd, kd, vd = dev_in[b]
-        if ulysses_mode:
+        if ulysses_mode and exch is not None:  # shards registered once: stage through them
+            for x_s, x_d in zip((ql, kl, vl), (qd, kd, vd)):
+                x_s.copy_(x_d)
+            exch.fused_run_step(dims, params, sched, cache, layer=0, step=0)
+            dev_out[b].copy_(ol)
+        elif ulysses_mode:
             dev_out[b].copy_(ulysses.ulysses_run_step(qd, kd, vd, dims, params, sched, cache, layer=0, step=0)[0])
         else:
             dfs.run_step(qd, kd, vd, dims, params, sched, cache, layer=0, step=0, out=dev_out[b])
@@ -626,7 +638,8 @@ def main():
     d2h = src[0].numel() * src[0].element_size() * world
     e2e = {"value": dense_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_call": e2e_ms,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "how": "public API dfs.run_step" + (" under ulysses_run_step" if ulysses_mode else "") +
+           "how": "public API dfs.run_step" + ((" under ulysses_run_step (NCCL)" if args.ulysses_nccl else
+                                                 " under PeerExchange.fused_run_step") if ulysses_mode else "") +
                   " on device copies of pinned host inputs, output read back every step; uploads/downloads of "
                   "neighbouring steps overlap on copy streams"}
 
@@ -650,7 +663,9 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic smooth Gaussian video fields (4 smoothing rounds), generated on device",
         "config": {"workload": wl["name"], "tokens": n, "heads": H, "heads_per_gpu": hl, "d": d, "block": B,
-                   "sub_block": Bs, "gamma": gamma, "K": K, "M": m, "parallelism": (f"ulysses all-to-all x{world}" if ulysses_mode else f"head-shard x{world}"),
+                   "sub_block": Bs, "gamma": gamma, "K": K, "M": m, "parallelism": ((f"ulysses NCCL all-to-all x{world}" if args.ulysses_nccl else
+                                    f"ulysses all-to-all fused into K2/K5 (P2P) x{world}") if ulysses_mode
+                                   else f"head-shard x{world}"),
                    "l2": "inputs 3x730 MB bf16 > 126 MB L2 (no flush needed)"},
         "ms_per_call_mask_reuse": t_reuse,
         "order_K1_ms_per_geometry": t_k1,

@@ -201,6 +201,32 @@ int dfs_mask_cache_size(dfs_handle* h, int64_t* n);
  * update step (any pointer may be NULL). DFS_E_INVALID when absent. */
 int dfs_mask_cache_info(dfs_handle* h, int layer, int head, int64_t* m, int64_t* block, int* last_update_step);
 
+/* Optional prologue fused into K2 (§8(f) row 1; PAPER.md:852 — the paper's end-to-end
+ * runs use fused QK-norm / RoPE kernels): each (token, head) row of q and of k is
+ * RMS-normalised over d, x * weight / sqrt(mean(x^2) + eps), then rotated by RoPE, in
+ * the same pass that reorders and pools it — so the DiT's separate norm / rotary pass
+ * over q and k (read + write of both tensors) disappears. The transformed rows are
+ * rounded to bf16 and are what the step scores and attends. */
+enum dfs_rope_layout {
+  DFS_ROPE_NONE = 0,
+  DFS_ROPE_INTERLEAVED = 1, /* pairs (2i, 2i+1) rotated by angle i (complex-multiply form) */
+  DFS_ROPE_HALF = 2         /* pairs (i, i + d/2) (rotate_half form) */
+};
+typedef struct {
+  const float* q_norm_weight; /* device [d] fp32, or NULL: q is not normalised */
+  const float* k_norm_weight; /* device [d] fp32, or NULL */
+  float eps;                  /* RMSNorm epsilon */
+  int rope_layout;            /* dfs_rope_layout */
+  const float* rope_cos;      /* device [N, d/2] fp32 by raster token (3D RoPE tables), or NULL */
+  const float* rope_sin;      /* device [N, d/2] fp32 */
+} dfs_qk_prologue;
+
+/* The prologue alone: q (which = 0, q_norm_weight) or k (which = 1, k_norm_weight) bf16
+ * [N, H, d] raster -> dst bf16, row i = transformed source row idx[i] (idx NULL: raster),
+ * in dst_layout. */
+int dfs_qk_prologue_apply(const dfs_qk_prologue* p, int which, const void* src, void* dst, int dst_layout,
+                          const uint32_t* idx, int64_t n, int64_t heads, int64_t d, dfs_stream stream);
+
 /* scheduler.cpp:91-135 run_step for ALL heads of one layer at once.
  * q, k, v, o: [N, H, d] bf16 raster-order activations (the DiT layout).
  * Dense steps (warmup or force_dense) run full attention in raster order;
@@ -244,6 +270,7 @@ typedef struct {
    * through K5, output converted back to fp32). */
   int dtype;
   int64_t dv; /* head dim of v / o; 0 = d (dv != d: DFS_F32 with n <= DFS_COMPAT_MAX_ROWS only) */
+  const dfs_qk_prologue* prologue; /* host pointer or NULL; bf16 steps with d % 16 == 0 only */
 } dfs_step_args;
 int dfs_run_step(dfs_handle* h, const dfs_schedule* s, const dfs_step_args* a, dfs_stream stream);
 

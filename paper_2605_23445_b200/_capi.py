@@ -19,6 +19,7 @@ DFS_OK, DFS_E_INVALID, DFS_E_RANGE, DFS_E_UNSUPPORTED, DFS_E_CUDA, DFS_E_INTERNA
 DFS_BF16, DFS_F32 = 0, 1
 DFS_NHD, DFS_HND = 0, 1
 DFS_OPT_GENERIC_SCORE, DFS_OPT_GENERIC_ATTN = 1, 2
+ROPE_LAYOUTS = {"none": 0, "interleaved": 1, "half": 2}
 ORDERINGS = {"raster": 0, "hilbert2d": 1, "block3d": 2, "hilbert3d": 3}
 
 if not os.path.exists(LIB_PATH):
@@ -69,7 +70,12 @@ class StepArgs(C.Structure):
                 ("sub_block", _i64), ("layer", _i32), ("step", _i32), ("force_dense", _i32),
                 ("nonfinite", _p), ("dense_out", C.POINTER(_i32)), ("budget_out", C.POINTER(_dbl)),
                 ("updated_out", C.POINTER(_i32)), ("sparsity_out", C.POINTER(_dbl)),
-                ("recall_out", C.POINTER(_dbl)), ("dtype", _i32), ("dv", _i64)]
+                ("recall_out", C.POINTER(_dbl)), ("dtype", _i32), ("dv", _i64), ("prologue", _p)]
+
+
+class QkPrologueArgs(C.Structure):
+    _fields_ = [("q_norm_weight", _p), ("k_norm_weight", _p), ("eps", _f), ("rope_layout", _i32),
+                ("rope_cos", _p), ("rope_sin", _p)]
 
 
 _SIGS = {
@@ -100,6 +106,7 @@ _SIGS = {
     "dfs_mask_cache_size": (_i32, [_p, C.POINTER(_i64)]),
     "dfs_mask_cache_info": (_i32, [_p, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32)]),
     "dfs_cast": (_i32, [_p, _i32, _p, _i32, _i64, _p, _p]),
+    "dfs_qk_prologue_apply": (_i32, [_p, _i32, _p, _p, _i32, _p, _i64, _i64, _i64, _p]),
     "dfs_alltoall_export": (_i32, [_p, C.POINTER(PeerHandle)]),
     "dfs_alltoall_import": (_i32, [C.POINTER(PeerHandle), C.POINTER(_p)]),
     "dfs_alltoall_close": (_i32, [_p]),

@@ -1,30 +1,16 @@
-// attn_sm100.cu — K5: block-sparse FlashAttention forward on tcgen05 / TMEM / TMA.
+// attn_b64.cu — K5 for B = 64: block-sparse FlashAttention forward on tcgen05 / TMEM / TMA
+// with 64-token query and key blocks (SURVEY §8(b) contract B in {64, 128}; config T).
 //
-// block_sparse_attention (attention.cpp:125-159) for B = 128 (B = 64: attn_b64.cu), d in {64, 128},
-// bf16 I/O, fp32 softmax and accumulation. Persistent CTAs (one per SM) walk
-// (head, query block) tiles; a tile visits ONLY the key blocks of its CSR list
-// (top-K LUT, or every block for dense / cross attention), so masked blocks
-// cost neither bytes nor FLOPs.
-//
-// Warp roles (64 + 128 * kWG threads; kWG = 2 -> 320):
-//   warp 0      TMA producer: Q tile (TMA tile::gather4 of raster rows when the
-//               reorder is fused), then K_0, K_1, K_2, V_0, K_3, V_1, ... into a
-//               ring of kStages smem slots (SWIZZLE_128B boxes of 128 x 64).
-//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into one of three
-//               TMEM S buffers (QK runs two blocks ahead of PV, so the tensor pipe
-//               always has work queued behind each PV), then O += P_j V_j with P_j
-//               read straight from TMEM (bf16, aliasing S_j) and O resident in TMEM.
-//   warps 2..   softmax / correction / epilogue: kWG warpgroups split the 128 key
-//               columns of every query row (TMEM lane); each thread handles
-//               128 / kWG logits per block and the row max is exchanged through
-//               shared memory with one named barrier per block. Online softmax in
-//               the log2 domain, exp2 split between MUFU and an FMA-pipe polynomial;
-//               O is rescaled in TMEM only when the running max grows by > 2^8 (the
-//               final normalisation uses the same stale max for O and l, so this is
-//               exact). The epilogue writes each output row straight to its raster
-//               position out_rows[i] — the unpermute (scheduler.cpp:134) is fused here.
-// Padded keys of the last partial block get -inf logits; padded query rows
-// are computed on TMA zero-fill and never stored (attention.cpp:146-152).
+// block_sparse_attention (attention.cpp:125-159) at B = 64 with the B = 128 kernel's
+// machinery (attn_sm100.cu: warp roles, TMA ring, three TMEM S buffers, online softmax
+// split over two warpgroups, fused unpermute): a 128-row tile holds the two query blocks
+// 2t and 2t+1 (one M = 128 MMA), and walks the UNION of their key lists in 64-key blocks
+// (N = 64 MMAs). A pre-pass merges the two ascending CSR rows into one list whose
+// entries carry an ownership mask (bit 28: block 2t, bit 29: block 2t+1); the softmax
+// warps of a half that does not own a block write P = 0 for it, so each query row
+// attends exactly its own block list (padded keys of the last block excluded, rows past
+// N never stored). Kept as a separate kernel so the B = 128 kernel's code stays the
+// tuned one (the generalised template measured +2.9 % SM cycles at HY, ncu).
 #include <cuda.h>
 
 #include <cstdio>
@@ -40,12 +26,14 @@ namespace {
 using namespace sm100;
 
 constexpr int kBM = 128;         // query rows per tile (= TMEM lanes)
-constexpr int kBN = 128;         // keys per block
+// Key block = MMA N: 128 (B = 128), or 64 (B = 64: a tile then holds the two query blocks
+// 2t, 2t+1 and walks the union of their key lists; each entry carries an ownership
+// mask in bits 28-29 and the rows of a half that does not own a block get P = 0).
+constexpr int32_t kBlkMask = 0x0fffffff;
 #ifndef DFS_ATTN_WG
 #define DFS_ATTN_WG 2
 #endif
 constexpr int kWG = DFS_ATTN_WG;           // softmax warpgroups splitting the 128 key columns
-constexpr int kCPT = 128 / kWG;            // key columns (logits) per softmax thread per block
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr uint32_t kTmemCols = 512;
@@ -55,18 +43,22 @@ constexpr uint32_t kTmemCols = 512;
 constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
 constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-row group (0 = __syncthreads)
 
-template <int D>
+template <int D, int BN>
 struct Cfg {
+  static constexpr int kBN = BN;
+  static constexpr int kCPT = BN / kWG;                  // key columns (logits) per softmax thread per block
   static constexpr int kChunks = D / 64;                 // 128-byte swizzle chunks per row
-  static constexpr int kTileBytes = kBM * D * 2;         // one Q / K / V tile
-  static constexpr int kChunkBytes = kBM * 128;          // one 128 x 64 bf16 TMA box
-  static constexpr int kStages = D == 64 ? 12 : 5;
+  static constexpr int kTileBytes = kBM * D * 2;         // the Q tile
+  static constexpr int kChunkBytes = kBM * 128;          // one 128 x 64 bf16 TMA box (Q)
+  static constexpr int kKVTileBytes = BN * D * 2;        // one K / V block
+  static constexpr int kKVChunkBytes = BN * 128;         // one BN x 64 bf16 TMA box (K / V)
+  static constexpr int kStages = D == 64 ? 12 : (BN == 128 ? 5 : 10);
   static constexpr int kQOff = 0;
   static constexpr int kRingOff = kQOff + kTileBytes;
-  static constexpr int kRedOff = kRingOff + kStages * kTileBytes;   // float max[2][kWG][128], sum[kWG][128]
+  static constexpr int kRedOff = kRingOff + kStages * kKVTileBytes;  // float max[2][kWG][128], sum[kWG][128]
   static constexpr int kBarOff = kRedOff + 3 * kWG * kBM * 4;
   static constexpr int kSmem = kBarOff + 512 + 1024;     // barriers + alignment slack
-  static constexpr uint32_t kIdescQK = idesc_bf16_f32(kBM, kBN, false, false);
+  static constexpr uint32_t kIdescQK = idesc_bf16_f32(kBM, BN, false, false);
   static constexpr uint32_t kIdescPV = idesc_bf16_f32(kBM, D, false, true);
   static constexpr int kSBufs = 3;         // TMEM: S0/P0 [0,128) S1/P1 [128,256) S2/P2 [256,384) O [384,384+D)
   static constexpr uint32_t kOCol = 384;
@@ -84,9 +76,9 @@ struct Params {
   int in_nhd;  // 1: inputs are [N, H, d] (tensor-map coordinates (col, head, row))
   float scale_log2;
   const uint32_t* in_rows;  // fused Q reorder: logical query row i = raster token in_rows[i] (NULL: tiles)
-  unsigned long long* trace;  // debug timeline (DFS_ATTN_TRACE), NULL in production
+  int64_t mq_blk;           // B = 64: query blocks per head (two per tile)
+  const int32_t* u_cnt;     // B = 64: per tile, the length of the union list at blk_idx[blk_ptr[h*mq_blk+2t]]
   int64_t tiles;
-  const dfs_peer_table* out_peers;  // Ulysses: rows go to the token owner's shard (kPeerOut instantiation)
 };
 
 struct Bars {
@@ -103,10 +95,15 @@ struct Bars {
 struct TileMeta {
   int32_t beg, cnt;
 };
+template <int BN>
 __device__ __forceinline__ TileMeta load_meta(const Params& p, int64_t tile) {
   TileMeta t{0, 0};
   if (tile < p.tiles) {
-    if (p.blk_ptr) {
+    if (p.blk_ptr && BN == 64) {  // union list of query blocks 2t, 2t+1, stored over their CSR rows
+      const int64_t h = tile / p.mq, u = tile - h * p.mq;
+      t.beg = __ldg(p.blk_ptr + h * p.mq_blk + 2 * u);
+      t.cnt = __ldg(p.u_cnt + tile);
+    } else if (p.blk_ptr) {
       t.beg = __ldg(p.blk_ptr + tile);
       t.cnt = __ldg(p.blk_ptr + tile + 1) - t.beg;
     } else {
@@ -116,13 +113,6 @@ __device__ __forceinline__ TileMeta load_meta(const Params& p, int64_t tile) {
   return t;
 }
 
-#ifdef DFS_ATTN_TRACE_BUILD
-__device__ __forceinline__ void trace(const Params& p, int ev, uint32_t idx) {
-  if (p.trace && blockIdx.x == 0 && idx < 256) p.trace[ev * 256 + idx] = clock64();
-}
-#else
-__device__ __forceinline__ void trace(const Params&, int, uint32_t) {}
-#endif
 
 __device__ __forceinline__ int32_t block_at(const Params& p, int32_t beg, int32_t j) {
   return p.blk_ptr ? p.blk_idx[beg + j] : j;
@@ -141,11 +131,13 @@ __device__ __forceinline__ constexpr bool use_poly(int i) {
   }
 }
 
-template <int D, int POLY, bool kPeerOut>
+template <int D, int POLY, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+    attn_b64_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const Params p) {
-  using C = Cfg<D>;
+  using C = Cfg<D, BN>;
+  constexpr int kBN = BN;
+  constexpr int kCPT = C::kCPT;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offset, so the pointer keeps its shared state space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -204,7 +196,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     auto issue_tile = [&](const CUtensorMap* map, int64_t h, int64_t row0, uint8_t* dst, uint64_t* bar,
-                          const int (&rr)[4], bool gather) {
+                          const int (&rr)[4], bool gather, uint32_t bytes, uint32_t chunk_bytes) {
+      if constexpr (BN == 128) {  // Q and K/V tiles share one geometry
+        bytes = C::kTileBytes;
+        chunk_bytes = C::kChunkBytes;
+      }
       if (gather) {
         if (elect_one()) mbar_expect_tx(bar, C::kTileBytes);
         __syncwarp();
@@ -215,10 +211,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         return;
       }
       if (elect_one()) {
-        mbar_expect_tx(bar, C::kTileBytes);
+        mbar_expect_tx(bar, bytes);
 #pragma unroll
         for (int c = 0; c < C::kChunks; ++c)
-          tma_load_3d(dst + c * C::kChunkBytes, map, bar, c * 64, p.in_nhd ? int(h) : int(row0),
+          tma_load_3d(dst + c * chunk_bytes, map, bar, c * 64, p.in_nhd ? int(h) : int(row0),
                       p.in_nhd ? int(row0) : int(h));
       }
       __syncwarp();
@@ -228,25 +224,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t use = ring / C::kStages;
       const int rr[4] = {0, 0, 0, 0};
       mbar_wait(&bars->kv_empty[slot], (use & 1) ^ 1);
-#ifdef DFS_ATTN_SKIP_TMA  // experiment builds only: K/V never loaded (garbage operands)
-      if (elect_one()) mbar_arrive(&bars->kv_full[slot]);
-      __syncwarp();
-#else
-      issue_tile(map, h, row0, sRing + slot * C::kTileBytes, &bars->kv_full[slot], rr, false);
-#endif
+      issue_tile(map, h, row0, sRing + slot * C::kKVTileBytes, &bars->kv_full[slot], rr, false, C::kKVTileBytes,
+                 C::kKVChunkBytes);
       ++ring;
     };
-    TileMeta nxt = load_meta(p, blockIdx.x);
+    TileMeta nxt = load_meta<BN>(p, blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
       const int64_t h = tile / p.mq, u = tile % p.mq;
       const int32_t beg = nxt.beg, cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta<BN>(p, tile + gridDim.x);
       {
         int rr[4] = {0, 0, 0, 0};
         if (p.in_rows) gather_rows(h, u * kBM, rr);  // row indices fetched while Q's slot drains
         mbar_wait(&bars->q_empty, q_phase ^ 1);
         q_phase ^= 1;
-        issue_tile(&tm_q, h, u * kBM, sQ, &bars->q_full, rr, p.in_rows != nullptr);
+        issue_tile(&tm_q, h, u * kBM, sQ, &bars->q_full, rr, p.in_rows != nullptr, C::kTileBytes, C::kChunkBytes);
       }
       // key-block list window: entries [win, win + 32) held one per lane
       int32_t win = -64, lut_reg = 0;
@@ -257,7 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           win = w;
           lut_reg = (w + lane < cnt) ? p.blk_idx[beg + w + lane] : 0;
         }
-        return __shfl_sync(0xffffffffu, lut_reg, j & 31);
+        const int32_t e = __shfl_sync(0xffffffffu, lut_reg, j & 31);
+        return BN == 64 ? e & kBlkMask : e;
       };
       // consumption order of the MMA warp (QK runs two blocks ahead of PV):
       // K0, K1, K2, V0, K3, V1, ..., K_{n-1}, V_{n-3}, V_{n-2}, V_{n-1}
@@ -279,12 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kHiK = desc_sw128_hi(1024);  // K-major SW128: LBO 16 B (unused), SBO 1024 B
     const uint32_t q_lo = desc_sw128_lo(smem_u32(sQ), 16);
     const uint32_t ring_lo = desc_sw128_lo(smem_u32(sRing), 16);
-    const uint32_t ring_lo_v = desc_sw128_lo(smem_u32(sRing), C::kChunkBytes);  // V: MN-major, LBO = chunk
+    const uint32_t ring_lo_v = desc_sw128_lo(smem_u32(sRing), C::kKVChunkBytes);  // V: MN-major, LBO = chunk
     auto next_slot = [&]() -> uint32_t {
       const uint32_t slot = ring % C::kStages;
-      trace(p, 0, ring);
       mbar_wait(&bars->kv_full[slot], (ring / C::kStages) & 1);
-      trace(p, 1, ring);
       ++ring;
       return slot;
     };
@@ -295,14 +286,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t slot = next_slot();
       const uint32_t sb = s_iter % C::kSBufs;
       tc_fence_after();
-      const uint32_t k_lo = ring_lo + slot * (C::kTileBytes >> 4);
+      const uint32_t k_lo = ring_lo + slot * (C::kKVTileBytes >> 4);
       if (elect_one()) {
 #pragma unroll
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
-#ifndef DFS_ATTN_SKIP_MMA  // experiment builds only (tools/attn_exp.sh): isolate the softmax side
-          umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off, kHiK, C::kIdescQK, s > 0);
-#endif
+          const uint32_t off_k = ((s >> 2) * C::kKVChunkBytes + (s & 3) * 32) >> 4;
+          umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off_k, kHiK, C::kIdescQK, s > 0);
         }
         umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->s_full[sb]);
@@ -313,19 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&](bool first) {
       const uint32_t slot = next_slot();
       const uint32_t pb = pv_iter % C::kSBufs;
-      trace(p, 2, pv_iter);
       mbar_wait(&bars->p_full[pb], (pv_iter / C::kSBufs) & 1);
-      trace(p, 3, pv_iter);
       tc_fence_after();
-      const uint32_t v_lo = ring_lo_v + slot * (C::kTileBytes >> 4);
+      const uint32_t v_lo = ring_lo_v + slot * (C::kKVTileBytes >> 4);
       const uint32_t p_tmem = tmem + pb * 128;  // P_j aliases S_j (bf16 pairs)
       if (elect_one()) {
 #pragma unroll
         for (int s = 0; s < kBN / 16; ++s) {
-#ifndef DFS_ATTN_SKIP_MMA
           umma_ts(tmem + C::kOCol, p_tmem + s * 8, v_lo + ((s * 16 * 128) >> 4), kHiK, C::kIdescPV,
                   (!first || s > 0) ? 1u : 0u);
-#endif
         }
         umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->o_done[pb]);
@@ -333,10 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       ++pv_iter;
     };
-    TileMeta nxt = load_meta(p, blockIdx.x);
+    TileMeta nxt = load_meta<BN>(p, blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
       const int32_t cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta<BN>(p, tile + gridDim.x);
       mbar_wait(&bars->q_full, q_phase);
       q_phase ^= 1;
       if (cnt > 0) issue_qk();
@@ -373,36 +359,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     // PV_{g-3} completed (in-order tcgen05 pipe, QK_{g+1} is issued after PV_{g-2}), so the
     // barrier is never more than one phase behind the one waited for.
     auto wait_pv = [&](uint32_t g) { mbar_wait(&bars->o_done[g % C::kSBufs], (g / C::kSBufs) & 1); };
-    TileMeta nxt = load_meta(p, blockIdx.x);
+    TileMeta nxt = load_meta<BN>(p, blockIdx.x);
     int32_t vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
+    // B = 64: rows 0-63 (warps & 3 in {0, 1}) are query block 2t (ownership bit 0), rows
+    // 64-127 query block 2t+1 (bit 1)
+    const int own_bit = ((warp & 3) >> 1) + 28;
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
       const int64_t h = tile / p.mq, u = tile % p.mq;
       const int32_t beg = nxt.beg, cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta<BN>(p, tile + gridDim.x);
       const int64_t i_row = u * kBM + r;  // this thread's query row, and its raster slot
       const int64_t orow = i_row < p.nq && p.out_rows ? int64_t(__ldg(p.out_rows + i_row)) : i_row;
       float m = -INFINITY;
       uint64_t lsum[2] = {0, 0};  // packed fp32x2 partial row sums (2 independent chains)
       int32_t vb_next = vb_first;
       for (int32_t j = 0; j < cnt; ++j) {
-        const int32_t vb = vb_next;
+        const int32_t entry = vb_next;
+        const int32_t vb = BN == 64 ? entry & kBlkMask : entry;
         if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);  // prefetch: keeps the LUT load off the critical path
         const uint32_t sb = s_iter % C::kSBufs;
         const uint32_t s_phase = (s_iter / C::kSBufs) & 1;
         float* red_par = red_max + (s_iter & 1) * kWG * kBM;
-        const bool tr = (threadIdx.x == 64 || threadIdx.x == 192);
-        if (tr) trace(p, 4 + (wg & 1) * 4, s_iter);
         mbar_wait(&bars->s_full[sb], s_phase);
-        if (tr) trace(p, 5 + (wg & 1) * 4, s_iter);
         tc_fence_after();
-#ifdef DFS_ATTN_SKIP_SOFTMAX  // experiment builds only: isolate the MMA/TMA side
-        (void)red_par;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
-        ++s_iter;
-        continue;
-#endif
+        if (BN == 64 && p.blk_ptr && !((entry >> own_bit) & 1)) {
+          // a block of the partner query block only: this half's P is zero (warp-uniform;
+          // the partner warps of these rows skip it the same way, so no exchange)
+          uint32_t zero[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) zero[i] = 0u;
+#pragma unroll
+          for (int c = 0; c < kCPT / 32; ++c) tmem_st16(tmem + lane_addr + sb * 128 + wg * (kCPT / 2) + c * 16, zero);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+          ++s_iter;
+          continue;
+        }
         uint32_t sv[kCPT];
 #pragma unroll
         for (int c = 0; c < kCPT / 32; ++c)
@@ -421,13 +415,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
         red_par[wg * kBM + r] = mx;
         named_bar_sync(bar_rows, kWG * 32);            // every slice of these rows published its max
-        if (tr) trace(p, 6 + (wg & 1) * 4, s_iter);
 #pragma unroll
         for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
         const float m_new = fmaxf(m, mx * p.scale_log2);
         // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
         // (the partner warps cover the same rows, so they decide identically)
-        if (j == 0) {
+        if (j == 0 || (BN == 64 && m == -INFINITY)) {  // first block this row attends
           m = m_new;
         } else if (__any_sync(0xffffffffu, m_new - m > kRescaleThreshold)) {
           wait_pv(s_iter - 1);                          // PV_{j-1} complete: O stable
@@ -481,7 +474,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     *reinterpret_cast<const uint32_t(*)[16]>(pk + 16 * c));
         tmem_wait_st();
         tc_fence_before();
-        if (tr) trace(p, 7 + (wg & 1) * 4, s_iter);
         __syncwarp();  // every lane's P store has completed (tcgen05.wait::st above)
         if (lane == 0) mbar_arrive(&bars->p_full[sb]);
         ++s_iter;
@@ -505,7 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t i = i_row;
       // an empty key list (possible only through a caller-built CSR; the BlockMask entry
       // points refuse it like attention.cpp:133-136) yields a zero row, never stale TMEM
-      const float inv_l = cnt > 0 ? 1.f / l_tot : 0.f;
+      // (B = 64: a half that owns none of the tile's blocks also gets a zero row)
+      const float inv_l = cnt > 0 && (BN == 128 || l_tot > 0.f) ? 1.f / l_tot : 0.f;
       constexpr int kOC = C::kOColsPerWG;
       uint32_t ov[kOC];
       if constexpr (kOC >= 32) {
@@ -522,14 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kOC; ++c) ov[c] = 0u;
       }
       if (i < p.nq) {
-        __nv_bfloat16* dst;
-        if constexpr (kPeerOut) {
-          const int64_t nl = p.out_peers->n_local, r = orow / nl;
-          dst = static_cast<__nv_bfloat16*>(const_cast<void*>(p.out_peers->ptr[r])) +
-                ((orow - r * nl) * p.out_peers->heads_total + p.out_peers->h0 + h) * D + wg * kOC;
-        } else {
-          dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
-        }
+        __nv_bfloat16* dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
 #pragma unroll
         // 32-byte stores (STG.256): half the store instructions of 16-byte ones; the store
         // issue at the tile boundary is what holds the warps there
@@ -537,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < kOC / 2; ++c)
           w[c] = pack_bf16(__uint_as_float(ov[2 * c]) * inv_l, __uint_as_float(ov[2 * c + 1]) * inv_l);
-        if (!kPeerOut && p.out_v8) {
+        if (p.out_v8) {
 #pragma unroll
           for (int q = 0; q < kOC / 16; ++q)
             asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + q * 16),
@@ -560,80 +546,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---- host ------------------------------------------------------------------------
 
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+}  // namespace
 
-EncodeFn get_encode() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(ptr);
-  }
-  return fn;
-}
+int make_token_map_rows(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t heads, int64_t d,
+                        int box_rows);  // attn_sm100.cu
+int make_row_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_t d);
 
-// 3D map over a token tensor so that box (64 cols, 128 rows, 1 head) is one
-// SWIZZLE_128B operand chunk; rows past n are zero-filled.
-int make_map(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t heads, int64_t d,
-             int box_rows = 128) {
-  EncodeFn enc = get_encode();
-  if (!enc) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3], strides[2];
-  cuuint32_t box[3], estr[3] = {1, 1, 1};
-  if (layout == DFS_HND) {  // [H, N, d]: dims (d, N, H)
-    dims[0] = cuuint64_t(d);
-    dims[1] = cuuint64_t(n);
-    dims[2] = cuuint64_t(heads);
-    strides[0] = cuuint64_t(d) * 2;
-    strides[1] = cuuint64_t(n) * cuuint64_t(d) * 2;
-    box[0] = 64;
-    box[1] = cuuint32_t(box_rows);
-    box[2] = 1;
-  } else {  // [N, H, d]: dims (d, H, N), box (64, 1, 128)
-    dims[0] = cuuint64_t(d);
-    dims[1] = cuuint64_t(heads);
-    dims[2] = cuuint64_t(n);
-    strides[0] = cuuint64_t(d) * 2;
-    strides[1] = cuuint64_t(heads) * cuuint64_t(d) * 2;
-    box[0] = 64;
-    box[1] = 1;
-    box[2] = cuuint32_t(box_rows);
-  }
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled failed");
-  return DFS_OK;
-}
+namespace {
 
-// 2D map over rows x d bf16 for tile::gather4: box {64 columns, 1 row}, SWIZZLE_128B
-int make_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_t d) {
-  EncodeFn enc = get_encode();
-  if (!enc) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  if (rows >= (int64_t(1) << 31)) return fail(DFS_E_UNSUPPORTED, "attn_sm100: N*H too large for row gather");
-  cuuint64_t dims[2] = {cuuint64_t(d), cuuint64_t(rows)};
-  cuuint64_t strides[1] = {cuuint64_t(d) * 2};
-  cuuint32_t box[2] = {64, 1}, estr[2] = {1, 1};
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled (gather) failed");
-  return DFS_OK;
-}
-
-template <int D, int POLY, bool kPeerOut = false>
+template <int D, int POLY, int BN>
 int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const Params& p,
                   cudaStream_t stream) {
-  using C = Cfg<D>;
+  using C = Cfg<D, BN>;
   // per device and race-free: set on every launch (~1 us)
-  DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D, POLY, kPeerOut>,
+  DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_b64_kernel<D, POLY, BN>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int64_t grid = p.tiles < kNumSMs ? p.tiles : kNumSMs;
-  attn_sm100_kernel<D, POLY, kPeerOut><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
+  attn_b64_kernel<D, POLY, BN><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
   DFS_LAUNCH_CHECK("attn_sm100");
   return DFS_OK;
 }
@@ -646,119 +575,96 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
 template <int D>
 constexpr int kDefaultPoly = D == 128 ? 38 : 3;
 
-template <int D>
+// B = 64: the union of the key lists of query blocks 2t and 2t+1, written over their
+// (adjacent) CSR rows: entry = key block | ownership bits (28: block 2t, 29: block 2t+1).
+// One thread per tile, a linear merge of two ascending lists (attention.cpp:146-152's
+// per-block key sets, visited once for both blocks).
+__global__ void union_pairs_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx, int64_t heads,
+                                   int64_t mq_blk, int64_t tiles_per_head, int32_t* __restrict__ out,
+                                   int32_t* __restrict__ cnt) {
+  const int64_t tile = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (tile >= heads * tiles_per_head) return;
+  const int64_t h = tile / tiles_per_head, t = tile - h * tiles_per_head;
+  const int64_t u0 = h * mq_blk + 2 * t;
+  const int32_t ab = ptr[u0], ae = ptr[u0 + 1];
+  const bool has_b = 2 * t + 1 < mq_blk;
+  const int32_t bb = has_b ? ptr[u0 + 1] : 0, be = has_b ? ptr[u0 + 2] : 0;
+  int32_t i = ab, j = bb, o = ab;
+  while (i < ae || j < be) {
+    const int32_t va = i < ae ? idx[i] : INT32_MAX, vb = j < be ? idx[j] : INT32_MAX;
+    if (va == vb) {
+      out[o++] = va | (3 << 28);
+      ++i;
+      ++j;
+    } else if (va < vb) {
+      out[o++] = va | (1 << 28);
+      ++i;
+    } else {
+      out[o++] = vb | (2 << 28);
+      ++j;
+    }
+  }
+  cnt[tile] = o - ab;
+}
+
+template <int D, int BN = 128>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   CUtensorMap mq, mk, mv;
   int rc;
   if (a.in_rows) {  // Q: 2D row-gather map over the raster [N*H, d] activations
-    if ((rc = make_gather_map(&mq, a.q, a.nq * a.heads, D))) return rc;
-  } else if ((rc = make_map(&mq, a.q, a.in_layout, a.nq, a.heads, D))) {
+    if ((rc = make_row_gather_map(&mq, a.q, a.nq * a.heads, D))) return rc;
+  } else if ((rc = make_token_map_rows(&mq, a.q, a.in_layout, a.nq, a.heads, D, 128))) {
     return rc;
   }
-  if ((rc = make_map(&mk, a.k, a.in_layout, a.nk, a.heads, D))) return rc;
-  if ((rc = make_map(&mv, a.v, a.in_layout, a.nk, a.heads, D))) return rc;
+  if ((rc = make_token_map_rows(&mk, a.k, a.in_layout, a.nk, a.heads, D, BN))) return rc;
+  if ((rc = make_token_map_rows(&mv, a.v, a.in_layout, a.nk, a.heads, D, BN))) return rc;
   Params p;
   p.heads = a.heads;
   p.nq = a.nq;
   p.nk = a.nk;
   p.mq = ceil_div(a.nq, kBM);
-  p.mk = ceil_div(a.nk, kBN);
+  p.mk = ceil_div(a.nk, BN);
+  p.mq_blk = ceil_div(a.nq, BN);
+  p.u_cnt = nullptr;
+  int32_t* u_buf = nullptr;
+  if (BN == 64 && a.blk_ptr) {
+    // the union lists live at the CSR offsets of their first query block: buffers of nnz entries
+    int32_t nnz = 0;
+    DFS_CUDA_CHECK(cudaMemcpyAsync(&nnz, a.blk_ptr + a.heads * p.mq_blk, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                   stream));
+    DFS_CUDA_CHECK(cudaStreamSynchronize(stream));
+    DFS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&u_buf),
+                                   sizeof(int32_t) * size_t(nnz + 1 + p.mq * a.heads), stream));
+    int32_t* cnt = u_buf + nnz + 1;
+    const int64_t tiles = p.mq * a.heads;
+    union_pairs_kernel<<<unsigned(ceil_div(tiles, 128)), 128, 0, stream>>>(a.blk_ptr, a.blk_idx, a.heads, p.mq_blk,
+                                                                         p.mq, u_buf, cnt);
+    DFS_LAUNCH_CHECK("union_pairs");
+    p.u_cnt = cnt;
+  }
   p.blk_ptr = a.blk_ptr;
-  p.blk_idx = a.blk_idx;
+  p.blk_idx = u_buf ? u_buf : a.blk_idx;
   p.out_rows = a.out_rows;
   p.out = static_cast<__nv_bfloat16*>(a.o);
   p.out_layout = a.out_layout;
-  p.out_peers = static_cast<const dfs_peer_table*>(a.out_peers);
-  p.out_v8 = !a.out_peers && (reinterpret_cast<uintptr_t>(a.o) & 31) == 0;  // peer shards: 16-byte stores
+  p.out_v8 = (reinterpret_cast<uintptr_t>(a.o) & 31) == 0;
   p.in_nhd = a.in_layout == DFS_NHD;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.in_rows = a.in_rows;
   p.tiles = p.mq * a.heads;
-  p.trace = nullptr;
-#ifdef DFS_ATTN_TRACE_BUILD
-  const char* trace_path = getenv("DFS_ATTN_TRACE");
-  if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 16 * 256 * sizeof(unsigned long long)));
-  if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 16 * 256 * sizeof(unsigned long long), stream));
-#endif
-  static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly<D>;
-  if (a.out_peers) {  // Ulysses: the epilogue stores into the token owners' shards
-    rc = launch_kernel<D, kDefaultPoly<D>, true>(mq, mk, mv, p, stream);
-  } else {
-    switch (poly) {
-      case 0: rc = launch_kernel<D, 0>(mq, mk, mv, p, stream); break;
-      case 2: rc = launch_kernel<D, 2>(mq, mk, mv, p, stream); break;
-      case 3: rc = launch_kernel<D, 3>(mq, mk, mv, p, stream); break;
-      case 38: rc = launch_kernel<D, 38>(mq, mk, mv, p, stream); break;
-      default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
-    }
-  }
+  static_assert(BN == 64, "attn_b64 instantiates the 64-key-block kernel only");
+  rc = launch_kernel<D, kDefaultPoly<D>, 64>(mq, mk, mv, p, stream);
+  if (u_buf) cudaFreeAsync(u_buf, stream);
   if (rc) return rc;
-#ifdef DFS_ATTN_TRACE_BUILD
-  if (p.trace) {
-    unsigned long long host[16 * 256];
-    DFS_CUDA_CHECK(cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream));
-    DFS_CUDA_CHECK(cudaStreamSynchronize(stream));
-    if (FILE* f = fopen(trace_path, "wb")) {
-      fwrite(host, sizeof(host), 1, f);
-      fclose(f);
-    }
-    cudaFree(p.trace);
-  }
-#endif
   return DFS_OK;
 }
 
 }  // namespace
 
-// bf16 token-tensor maps shared with the recall kernel (recall_sm100.cu) and the B = 64
-// attention kernel (attn_b64.cu)
-int make_token_map(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t heads, int64_t d) {
-  return make_map(map, base, layout, n, heads, d);
-}
-int make_token_map_rows(CUtensorMap* map, const void* base, int layout, int64_t n, int64_t heads, int64_t d,
-                        int box_rows) {
-  return make_map(map, base, layout, n, heads, d, box_rows);
-}
-int make_row_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_t d) {
-  return make_gather_map(map, base, rows, d);
-}
-
-// [H, rows, d] fp16 operand map for the scorer (score_sm100.cu): box 64 x box_rows x 1, SW128
-int make_map_f16(CUtensorMap* map, const void* base, int64_t rows, int64_t heads, int64_t d, int box_rows) {
-  EncodeFn enc = get_encode();
-  if (!enc) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {cuuint64_t(d), cuuint64_t(rows), cuuint64_t(heads)};
-  cuuint64_t strides[2] = {cuuint64_t(d) * 2, cuuint64_t(rows) * cuuint64_t(d) * 2};
-  cuuint32_t box[3] = {64, cuuint32_t(box_rows), 1}, estr[3] = {1, 1, 1};
-  const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(DFS_E_CUDA, "cuTensorMapEncodeTiled (f16) failed");
-  return DFS_OK;
-}
-
-bool attn_sm100_supports(const dfs_attn_args& a) {
-  if (a.dtype != DFS_BF16 || (a.block != 128 && a.block != 64) || (a.d != 64 && a.d != 128)) return false;
-  if (a.dv > 0 && a.dv != a.d) return false;
-  if (a.in_rows && a.nq >= (int64_t(1) << 31) / a.heads) return false;
-  const void* ptrs[4] = {a.q, a.k, a.v, a.o};
-  for (const void* ptr : ptrs)
-    if (reinterpret_cast<uintptr_t>(ptr) & 15) return false;
-  if (a.nq >= (int64_t(1) << 31) || a.nk >= (int64_t(1) << 31)) return false;
-  return true;
-}
-
-int sparse_attn_b64(const dfs_attn_args& a, float scale, cudaStream_t stream);  // attn_b64.cu
-
-int sparse_attn_sm100(const dfs_attn_args& a, float scale, cudaStream_t stream) {
-  if (a.block == 64) {
-    if (a.out_peers) return fail(DFS_E_UNSUPPORTED, "attn_sm100: peer-scattered output needs B = 128");
-    return sparse_attn_b64(a, scale, stream);
-  }
-  if (a.block != 128) return fail(DFS_E_UNSUPPORTED, "attn_sm100: block must be 64 or 128");
-  if (a.d == 128) return launch<128>(a, scale, stream);
-  if (a.d == 64) return launch<64>(a, scale, stream);
-  return fail(DFS_E_UNSUPPORTED, "attn_sm100: d must be 64 or 128");
+int sparse_attn_b64(const dfs_attn_args& a, float scale, cudaStream_t stream) {
+  if (a.d == 128) return launch<128, 64>(a, scale, stream);
+  if (a.d == 64) return launch<64, 64>(a, scale, stream);
+  return fail(DFS_E_UNSUPPORTED, "attn_b64: d must be 64 or 128");
 }
 
 }  // namespace dfsgpu

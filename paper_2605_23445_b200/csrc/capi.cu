@@ -41,6 +41,9 @@ int cast_impl(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t 
 int permute_rows_peer_impl(const dfs_peer_table* peers_dev, int64_t heads_total, void* dst, const uint32_t* idx,
                            int64_t n, int64_t heads, int64_t d, float* pooled, int64_t pool, int32_t* nonfinite,
                            cudaStream_t stream);
+int prologue_permute_impl(const void* src, void* dst, int dst_layout, const uint32_t* idx, int64_t n, int64_t heads,
+                          int64_t d, float* pooled, int64_t pool, int32_t* nonfinite, const float* norm_weight,
+                          float eps, int rope_layout, const float* cos_t, const float* sin_t, cudaStream_t stream);
 int score_blocks_generic(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
                          int64_t sub_block, double* S, float* P_ws, int64_t P_ws_floats, cudaStream_t stream);
 int score_blocks_sm100(const float* pq, const float* pk, int64_t heads, int64_t n, int64_t d, int64_t block,
@@ -227,6 +230,15 @@ int attn_dispatch(dfs_handle* h, const dfs_attn_args& a, cudaStream_t stream) {
   if (a.out_peers && (a.force_generic || h->opt_generic_attn || !attn_sm100_supports(a)))
     return fail(DFS_E_UNSUPPORTED, "sparse_attn: peer-scattered output needs the tcgen05 kernel");
   if (!a.force_generic && !h->opt_generic_attn && attn_sm100_supports(a)) return sparse_attn_sm100(a, scale, stream);
+  // bf16 is the performance path: geometry outside the tcgen05 kernel's contract is an
+  // explicit refusal, never a silent ~20x slower SIMT fallback. The SIMT
+  // kernel serves fp32 (the drop-in Matrix path, fp64 arithmetic) and callers that ask
+  // for it (force_generic / DFS_OPT_GENERIC_ATTN).
+  if (a.dtype == DFS_BF16 && !a.force_generic && !h->opt_generic_attn)
+    return fail(DFS_E_UNSUPPORTED,
+                "sparse_attn: the bf16 tensor-core kernel needs B in {64, 128}, d in {64, 128}, dv == d and "
+                "16-byte aligned q/k/v/o (got B = " + std::to_string(a.block) + ", d = " + std::to_string(a.d) +
+                "); set force_generic / DFS_OPT_GENERIC_ATTN for the SIMT kernel");
   return sparse_attn_generic(a, scale, stream);
 }
 
@@ -681,6 +693,15 @@ int dfs_cast(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t c
   return cast_impl(src, src_dtype, dst, dst_dtype, count, nonfinite, as_stream(stream));
 }
 
+int dfs_qk_prologue_apply(const dfs_qk_prologue* p, int which, const void* src, void* dst, int dst_layout,
+                          const uint32_t* idx, int64_t n, int64_t heads, int64_t d, dfs_stream stream) {
+  if (!p || !src || !dst || (which != 0 && which != 1)) return fail(DFS_E_INVALID, "qk_prologue: bad arguments");
+  if (n < 1 || heads < 1 || d < 1) return fail(DFS_E_INVALID, "qk_prologue: empty input");
+  return prologue_permute_impl(src, dst, dst_layout, idx, n, heads, d, nullptr, 1, nullptr,
+                               which ? p->k_norm_weight : p->q_norm_weight, p->eps, p->rope_layout, p->rope_cos,
+                               p->rope_sin, as_stream(stream));
+}
+
 int dfs_mask_cache_info(dfs_handle* h, int layer, int head, int64_t* m, int64_t* block, int* last_update_step) {
   if (!h) return fail(DFS_E_INVALID, "null handle");
   auto it = h->masks.find(layer);
@@ -874,9 +895,39 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   if (n < 1 || H < 1 || d < 1) return fail(DFS_E_INVALID, "attention: empty input");
   if (Bs < 1 || B < Bs) return fail(DFS_E_INVALID, "ScoringParams: need 1 <= sub_block_size <= block_size");
   if (B % Bs) return fail(DFS_E_INVALID, "ScoringParams: sub_block_size must divide block_size");
-  const bool compat = dtype == DFS_F32 && n <= DFS_COMPAT_MAX_ROWS;
+  // the tcgen05 attention kernel's geometry contract, checked before anything runs
+  auto tc_ok = [&](const void* q, const void* k, const void* v, const void* o) {
+    dfs_attn_args pr{};
+    pr.q = q;
+    pr.k = k;
+    pr.v = v;
+    pr.o = const_cast<void*>(o);
+    pr.dtype = DFS_BF16;
+    pr.heads = H;
+    pr.nq = n;
+    pr.nk = n;
+    pr.d = d;
+    pr.dv = dv == d ? 0 : dv;
+    pr.block = B;
+    pr.in_rows = reinterpret_cast<const uint32_t*>(a->q);  // the sparse step gathers Q rows
+    return attn_sm100_supports(pr);
+  };
+  // fp32 inputs: compatibility kernels up to the cap, and for any geometry the tensor-core
+  // kernels do not cover (the drop-in Matrix API accepts every shape the reference does)
+  const bool compat = dtype == DFS_F32 && (n <= DFS_COMPAT_MAX_ROWS || dv != d || !tc_ok(h, h, h, h));
+  if (dtype == DFS_BF16 && !h->opt_generic_attn && !tc_ok(a->q, a->k, a->v, a->o))
+    return fail(DFS_E_UNSUPPORTED,
+                "run_step: bf16 steps run the tensor-core kernels (B in {64, 128}, d in {64, 128}, 16-byte aligned "
+                "[N, H, d] tensors); got B = " + std::to_string(B) + ", d = " + std::to_string(d) +
+                " (DFS_OPT_GENERIC_ATTN selects the SIMT kernel)");
   if (dv != d && !compat)
-    return fail(DFS_E_UNSUPPORTED, "run_step: dv != d only on the fp32 compatibility path (n <= 4096)");
+    return fail(DFS_E_UNSUPPORTED, "run_step: dv != d only on the fp32 compatibility path");
+  const dfs_qk_prologue* pro = a->prologue;
+  if (pro && (dtype != DFS_BF16 || d % 16))
+    return fail(DFS_E_UNSUPPORTED, "run_step: the QK-norm / RoPE prologue runs on bf16 steps with d % 16 == 0");
+  if (pro && pro->rope_layout != DFS_ROPE_NONE && pro->rope_layout != DFS_ROPE_INTERLEAVED &&
+      pro->rope_layout != DFS_ROPE_HALF)
+    return fail(DFS_E_INVALID, "run_step: unknown RoPE layout");
   double budget;
   if (int rc = dfs_schedule_budget_at(sched, a->step, &budget)) return rc;
   const int64_t m = ceil_div(n, B);
@@ -887,6 +938,11 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     flag = h->step_flag.as<int32_t>();
     DFS_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
   }
+  // q or k through the prologue: raster -> dst (reordered by idx, or raster for idx == NULL)
+  auto prologue = [&](const void* x, void* dst, int layout, const uint32_t* idx, float* pooled, const float* w) {
+    return prologue_permute_impl(x, dst, layout, idx, n, H, d, pooled, Bs, flag, w, pro->eps, pro->rope_layout,
+                                 pro->rope_cos, pro->rope_sin, s);
+  };
   const size_t tok16 = sizeof(__nv_bfloat16) * size_t(n * H * d);
   // fp32 inputs past the cap: bf16 copies for the tensor-core kernels (finite check folded in)
   auto cast_inputs = [&]() -> int {
@@ -900,7 +956,16 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   };
 
   if (budget < 0.0 || a->force_dense) {  // scheduler.cpp:99-105: dense, raster order, no reorder
-    if (dtype == DFS_BF16 || compat) {
+    if (pro) {  // normalised / rotated q and k in raster order, then dense attention
+      if ((rc = h->q16.ensure(tok16)) || (rc = h->k16.ensure(tok16))) return rc;
+      if ((rc = prologue(a->q, h->q16.p, DFS_NHD, nullptr, nullptr, pro->q_norm_weight)) ||
+          (rc = prologue(a->k, h->k16.p, DFS_NHD, nullptr, nullptr, pro->k_norm_weight)) ||
+          (rc = finite_check_impl(a->v, n * H * d, DFS_BF16, flag, s)) || (rc = check_flag(flag, s)))
+        return rc;
+      if ((rc = attn_simple(h, h->q16.p, h->k16.p, a->v, a->o, DFS_BF16, DFS_NHD, nullptr, DFS_NHD, nullptr, H, n, d,
+                            d, B, nullptr, nullptr, s)))
+        return rc;
+    } else if (dtype == DFS_BF16 || compat) {
       const int64_t c[3] = {n * H * d, n * H * d, n * H * dv};
       const void* x[3] = {a->q, a->k, a->v};
       for (int t = 0; t < 3; ++t)
@@ -1004,15 +1069,26 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       att_q = q;
       pq = pk = nullptr;  // already pooled
     }
-    if (pq) {
+    if (pro) {
+      // QK-norm / RoPE fused into the reorder: the transformed q gets a reordered copy
+      // (K5 then loads Q tiles instead of gathering raster rows), k goes to k_hnd
+      if ((rc = h->q16.ensure(tok16))) return rc;
+      if ((rc = prologue(q, h->q16.p, DFS_HND, fwd, pq, pro->q_norm_weight)) ||
+          (rc = prologue(k, h->k_hnd.p, DFS_HND, fwd, pk, pro->k_norm_weight)) ||
+          (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag, false, s)))
+        return rc;
+      att_q = h->q16.p;
+      k = v = nullptr;  // done
+    } else if (pq) {
       if ((rc = permute_rows_impl(q, DFS_NHD, nullptr, DFS_HND, DFS_BF16, fwd, n, H, d, pq, Bs, flag, false, s)))
         return rc;
     } else if (dtype == DFS_BF16 && (rc = finite_check_impl(q, n * H * d, DFS_BF16, flag, s))) {
       return rc;
     }
-    if ((rc = permute_rows_impl(k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, pk ? Bs : 1, flag,
-                                false, s)) ||
-        (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag, false, s)))
+    if (!pro && ((rc = permute_rows_impl(k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, pk ? Bs : 1,
+                                         flag, false, s)) ||
+                 (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag,
+                                         false, s))))
       return rc;
   }
   if ((rc = check_flag(flag, s))) return rc;  // nothing scored, cached or written yet
@@ -1031,7 +1107,7 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
                      L->ptr.as<int32_t>(), L->idx.as<int32_t>(), s);
     if (!rc) rc = cast_impl(h->o16.p, DFS_BF16, a->o, DFS_F32, n * H * d, nullptr, s);
   } else {
-    rc = attn_simple(h, att_q, att_k, att_v, a->o, DFS_BF16, DFS_HND, fwd, DFS_NHD, fwd, H, n, d, d, B,
+    rc = attn_simple(h, att_q, att_k, att_v, a->o, DFS_BF16, DFS_HND, pro ? nullptr : fwd, DFS_NHD, fwd, H, n, d, d, B,
                      L->ptr.as<int32_t>(), L->idx.as<int32_t>(), s);
   }
   if (rc) return rc;
@@ -1040,7 +1116,8 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     if (compat)
       rc = compat_recall(h, *L, h->f32_q.as<float>(), h->f32_k.as<float>(), H, n, d, a->recall_out, s);
     else
-      rc = dfs_block_recall(h, att_q, h->k_hnd.p, DFS_HND, fwd, H, n, d, L->ptr.as<int32_t>(), L->idx.as<int32_t>(),
+      rc = dfs_block_recall(h, att_q, h->k_hnd.p, DFS_HND, pro ? nullptr : fwd, H, n, d, L->ptr.as<int32_t>(),
+                            L->idx.as<int32_t>(),
                             a->recall_out, stream);
     if (rc) return rc;
   }

@@ -66,6 +66,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
   // independent 16-byte row loads in flight per thread: 4 keeps the pooling variant at
   // <= 56 registers (3 CTAs of 384 threads per SM); 8 or 16 cost more in occupancy than
   // they gain in memory-level parallelism (tools/permute_bench.py: 0.73 -> 0.69 ms at HY)
+  // (r2: 8 in flight for the pooling variants measured again — q pass 0.191 -> 0.213 ms, k pass
+  // 0.267 -> 0.284 ms at HY, tools/permute_bench.py — so 4 stays)
   constexpr int kBatch = 4;
   const int64_t vec_per_row = d / V;
   const int64_t slots = heads * vec_per_row;
@@ -266,7 +268,127 @@ __global__ void cast_bf16_f32_kernel(const __nv_bfloat16* __restrict__ src, floa
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
 
+// K2 with the QK-norm / RoPE prologue (dfs_qk_prologue): bf16 [N, H, d] raster rows,
+// RMS-normalised and rotated in registers, rounded to bf16, written to `dst` (reordered
+// [H, N, d], or raster [N, H, d] for a dense step) and pooled. One thread per (head,
+// 16-byte chunk) slot; a row's d/8 chunks sit in consecutive lanes, so the row's sum of
+// squares and the rotate_half partner exchange are warp shuffles.
+__global__ void __launch_bounds__(1024) prologue_kernel(const __nv_bfloat16* __restrict__ src,
+                                                       __nv_bfloat16* __restrict__ dst, int dst_layout,
+                                                       const uint32_t* __restrict__ idx, int64_t n, int64_t heads,
+                                                       int64_t d, int rows, float* __restrict__ pooled,
+                                                       int64_t pool, int32_t* __restrict__ nonfinite,
+                                                       const float* __restrict__ nw, float eps, int rope_layout,
+                                                       const float* __restrict__ cos_t,
+                                                       const float* __restrict__ sin_t) {
+  const int vpr = int(d / 8);  // 8 or 16 chunks per row: a power of two that divides 32
+  const int64_t slots = heads * vpr;
+  const int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x;
+  const bool active = s < slots;
+  const int64_t h = active ? s / vpr : 0;
+  const int c = int(s % vpr) * 8;
+  const int64_t r0 = int64_t(blockIdx.x) * rows;
+  __shared__ int64_t s_src[64], s_dst[64];
+  for (int t = threadIdx.x; t < rows; t += blockDim.x) {
+    const int64_t i = r0 + t;
+    int64_t si = -1;
+    if (i < n) si = idx ? int64_t(idx[i]) : i;
+    if (si >= n) si = -1;
+    s_src[t] = si;
+    s_dst[t] = si >= 0 ? i : -1;
+  }
+  __syncthreads();
+  float w[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w[j] = nw && active ? nw[c + j] : 1.f;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool bad = false;
+  const int half = int(d / 2);
+  for (int r = 0; r < rows; ++r) {
+    const int64_t si = s_src[r], di = s_dst[r];
+    if (si < 0) continue;  // CTA-uniform
+    const uint4 u = active ? __ldg(reinterpret_cast<const uint4*>(src + (si * heads + h) * d + c))
+                           : make_uint4(0u, 0u, 0u, 0u);
+    float x[8];
+    unpack<__nv_bfloat16>(u, x);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bad |= !isfinite(x[j]);
+    if (nw) {
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss = fmaf(x[j], x[j], ss);
+      for (int o = vpr / 2; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float rs = 1.f / sqrtf(ss / float(d) + eps);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) x[j] = x[j] * rs * w[j];
+    }
+    if (rope_layout == DFS_ROPE_INTERLEAVED) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float co = active ? __ldg(cos_t + si * half + c / 2 + i) : 0.f;
+        const float sn = active ? __ldg(sin_t + si * half + c / 2 + i) : 0.f;
+        const float a = x[2 * i], b = x[2 * i + 1];
+        x[2 * i] = a * co - b * sn;
+        x[2 * i + 1] = a * sn + b * co;
+      }
+    } else if (rope_layout == DFS_ROPE_HALF) {
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[j] = __shfl_xor_sync(0xffffffffu, x[j], vpr / 2);
+      const bool lo = c < half;
+      const int t0 = lo ? c : c - half;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float co = active ? __ldg(cos_t + si * half + t0 + j) : 0.f;
+        const float sn = active ? __ldg(sin_t + si * half + t0 + j) : 0.f;
+        x[j] = lo ? x[j] * co - y[j] * sn : x[j] * co + y[j] * sn;
+      }
+    }
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __nv_bfloat162 p2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+      pk[j] = *reinterpret_cast<const uint32_t*>(&p2);
+      if (pooled) {
+        acc[2 * j] += double(__low2float(p2));
+        acc[2 * j + 1] += double(__high2float(p2));
+      }
+    }
+    if (active && dst)
+      *reinterpret_cast<uint4*>(dst + row_offset(dst_layout, n, heads, d, h, di) + c) =
+          make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  if (pooled && active) {
+    float* out = pooled + (h * ceil_div(n, pool) + r0 / pool) * d + c;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[j] = float(acc[j] / double(pool));
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
 }  // namespace
+
+int prologue_permute_impl(const void* src, void* dst, int dst_layout, const uint32_t* idx, int64_t n, int64_t heads,
+                          int64_t d, float* pooled, int64_t pool, int32_t* nonfinite, const float* norm_weight,
+                          float eps, int rope_layout, const float* cos_t, const float* sin_t, cudaStream_t stream) {
+  if (d % 16 || d / 8 > 32) return fail(DFS_E_UNSUPPORTED, "qk prologue: d must be a multiple of 16, <= 256");
+  if ((pooled && (pool < 1 || pool > 64)) || (reinterpret_cast<uintptr_t>(src) & 15) ||
+      (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(DFS_E_UNSUPPORTED, "qk prologue: pool <= 64 and 16-byte aligned buffers");
+  if (rope_layout != DFS_ROPE_NONE && (!cos_t || !sin_t))
+    return fail(DFS_E_INVALID, "qk prologue: RoPE tables missing");
+  const int64_t rows = pooled ? pool : 16;
+  const int64_t grid = ceil_div(n, rows);
+  const int64_t slots = heads * (d / 8);
+  const int64_t ysplit = ceil_div(slots, 512);
+  const int threads = int(ceil_div(ceil_div(slots, ysplit), 32) * 32);
+  if (grid > int64_t(INT32_MAX) || ysplit > 65535) return fail(DFS_E_UNSUPPORTED, "qk prologue: too many rows");
+  prologue_kernel<<<dim3(unsigned(grid), unsigned(ysplit)), threads, 0, stream>>>(
+      static_cast<const __nv_bfloat16*>(src), static_cast<__nv_bfloat16*>(dst), dst_layout, idx, n, heads, d,
+      int(rows), pooled, pool, nonfinite, norm_weight, eps, rope_layout, cos_t, sin_t);
+  DFS_LAUNCH_CHECK("qk_prologue");
+  return DFS_OK;
+}
 
 // K2 over sequence-sharded peers (Ulysses): gather + pool + finite check of this rank's
 // head group, bf16 only, destination [heads, n, d] (HND) or NULL (read-only pooling pass)

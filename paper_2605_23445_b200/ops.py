@@ -624,9 +624,43 @@ class StepStats:  # scheduler.hpp:78-85 (per head)
     recall: list | None = None  # per head, when run_step(..., record_recall=True)
 
 
+@dataclass
+class QkPrologue:
+    """QK-norm + RoPE fused into K2 (dfs_qk_prologue): q and k rows are RMS-normalised over d
+    (x * weight / sqrt(mean(x^2) + eps)) and rotated by RoPE before they are reordered, pooled
+    and attended. Weights: fp32 CUDA [d] (None: no norm); rope_cos / rope_sin: fp32 CUDA
+    [N, d/2] by raster token; rope: "none" | "interleaved" (pairs 2i, 2i+1) | "half" (i, i+d/2)."""
+
+    q_norm_weight: torch.Tensor | None = None
+    k_norm_weight: torch.Tensor | None = None
+    eps: float = 1e-6
+    rope: str = "none"
+    rope_cos: torch.Tensor | None = None
+    rope_sin: torch.Tensor | None = None
+
+    def c_args(self):
+        for t in (self.q_norm_weight, self.k_norm_weight, self.rope_cos, self.rope_sin):
+            if t is not None and (not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous()):
+                raise ValueError("QkPrologue: weights and RoPE tables must be contiguous fp32 CUDA tensors")
+        if self.rope not in capi.ROPE_LAYOUTS:
+            raise ValueError(f"QkPrologue: unknown RoPE layout {self.rope}")
+        return capi.QkPrologueArgs(_ptr(self.q_norm_weight).value, _ptr(self.k_norm_weight).value, float(self.eps),
+                                   capi.ROPE_LAYOUTS[self.rope], _ptr(self.rope_cos).value,
+                                   _ptr(self.rope_sin).value)
+
+    def apply(self, x: torch.Tensor, which: str = "q") -> torch.Tensor:
+        """The prologue alone on bf16 [N, H, d] raster rows (q or k weights) -> bf16 [N, H, d]."""
+        n, h, d = x.shape
+        out = torch.empty_like(x)
+        a = self.c_args()
+        capi.call("dfs_qk_prologue_apply", C.byref(a), 0 if which == "q" else 1, _ptr(x), _ptr(out), capi.DFS_NHD,
+                  None, n, h, d, _stream())
+        return out
+
+
 def run_step(q, k, v, dims, params: ScoringParams, schedule: SparsitySchedule, cache: MaskCache, layer: int,
              step: int, force_dense: bool = False, perm: Permutation | None = None, out=None,
-             record_recall: bool = False):
+             record_recall: bool = False, prologue: QkPrologue | None = None):
     """scheduler.hpp:93 run_step for ALL heads of one layer: q, k, v [N, H, d] raster order.
 
     bf16 is the performance path; fp32 runs the compatibility kernels up to 4096 tokens
@@ -659,7 +693,10 @@ def run_step(q, k, v, dims, params: ScoringParams, schedule: SparsitySchedule, c
                       params.block_size, params.sub_block_size, layer, step, int(force_dense),
                       None, C.pointer(dense), C.pointer(budget),
                       C.cast(upd, C.POINTER(C.c_int)), C.cast(spars, C.POINTER(C.c_double)),
-                      C.cast(rec, C.POINTER(C.c_double)) if rec is not None else None, _dtype_code(q), dv)
+                      C.cast(rec, C.POINTER(C.c_double)) if rec is not None else None, _dtype_code(q), dv, None)
+    pro = prologue.c_args() if prologue is not None else None
+    if pro is not None:
+        a.prologue = C.cast(C.pointer(pro), C.c_void_p)
     with cache.lock:
         capi.call("dfs_run_step", cache.handle.ptr, C.byref(schedule._s), C.byref(a), _stream())
     stats = StepStats(bool(dense.value), budget.value, [bool(x) for x in upd], list(spars),

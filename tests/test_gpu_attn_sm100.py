@@ -255,3 +255,52 @@ def test_text_cross_attention_shapes(nk):
     qf, kf, vf = (x.float().transpose(0, 1) for x in (q, k, v))
     ref = (torch.softmax(qf @ kf.transpose(1, 2) / d ** 0.5, -1) @ vf).transpose(0, 1)
     assert rel(o.float(), ref) <= 2e-2
+
+
+def _random_csr(h, mq, mk, gen, kmax):
+    """Ragged per-row key lists (1..kmax blocks, ascending) as a CSR over (head, query block)."""
+    ptr, idx = [0], []
+    for _ in range(h * mq):
+        k = int(torch.randint(1, kmax + 1, (1,), generator=gen))
+        sel = torch.randperm(mk, generator=gen)[:k].sort().values
+        idx.append(sel)
+        ptr.append(ptr[-1] + len(sel))
+    return torch.tensor(ptr, dtype=torch.int32).cuda(), torch.cat(idx).to(torch.int32).cuda()
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("n", [64, 256, 1000, 4096 + 33])
+def test_sm100_block64_union_tiles(d, n):
+    """B = 64 on tensor cores: a 128-row tile holds query blocks 2t and 2t+1 and walks the
+    union of their (ragged, partly shared) key lists; each half attends only its own
+    blocks (P = 0 elsewhere). Odd block counts leave a tile with one real query block;
+    the partial last key block is masked (attention.cpp:146-152). vs the SIMT kernel."""
+    m = dfs()
+    gen = torch.Generator().manual_seed(n + d)
+    h = 2
+    q, kk, v = (torch.randn(h, n, d, generator=gen).to(torch.bfloat16).cuda() for _ in range(3))
+    mb = -(-n // 64)
+    ptr, idx = _random_csr(h, mb, mb, gen, kmax=min(mb, 6))
+    o_fast = m.sparse_attention_csr(q, kk, v, ptr, idx, 64)
+    o_ref = m.sparse_attention_csr(q, kk, v, ptr, idx, 64, force_generic=True)
+    torch.cuda.synchronize()
+    for hh in range(h):
+        assert rel(o_fast[hh].float(), o_ref[hh].float()) <= 1e-2, hh
+    # dense at B = 64 (full list, both halves own every block) and Nq != Nk
+    qn = q.transpose(0, 1).contiguous()
+    kn = torch.randn(n + 50, h, d, generator=gen).to(torch.bfloat16).cuda()
+    vn = torch.randn(n + 50, h, d, generator=gen).to(torch.bfloat16).cuda()
+    o = m.full_attention_output(qn, kn, vn, block=64)
+    og = m.full_attention_output(qn, kn, vn, block=64, force_generic=True)
+    assert rel(o.float(), og.float()) <= 1e-2
+
+
+def test_bf16_unsupported_geometry_is_refused():
+    """No silent SIMT fallback on the bf16 path: d = 96 or B = 32 raise
+    UnsupportedGeometry unless the caller asks for the SIMT kernel."""
+    m = dfs()
+    for n, d, b in ((300, 96, 128), (300, 64, 32)):
+        q = torch.randn(n, 2, d).to(torch.bfloat16).cuda()
+        with pytest.raises(m._capi.UnsupportedGeometry):
+            m.full_attention_output(q, q, q, block=b)
+        m.full_attention_output(q, q, q, block=b, force_generic=True)  # explicit opt-in runs

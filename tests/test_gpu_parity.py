@@ -335,8 +335,11 @@ def test_mask_cache_store_find_roundtrip():
 
 
 def test_trajectory_masks_match_reference(golden):
-    """cmd_run-style trajectory (commands.cpp:221-319): every cached mask of
-    every (step, layer, head) equals the reference's, outputs within bf16 tol."""
+    """cmd_run-style trajectory (commands.cpp:221-319) through the batched device step on
+    the reference's OWN fp32 inputs (dfs.run_step with fp32 [N, H, d]: the compatibility
+    kernels, fp64 softmax arithmetic): every (step, layer, head) dense / update flag and
+    every cached mask is bit-identical to the reference's, and the sparse outputs match the
+    oracle's attention under that mask at the reference's 1e-5 tolerance."""
     t = golden("trajectory")
     f, h_, w, d, L, H, T, b, bs = (int(x) for x in t["meta"])
     m = dfs()
@@ -347,6 +350,8 @@ def test_trajectory_masks_match_reference(golden):
     params = m.ScoringParams(b, bs)
     n = f * h_ * w
     mm = -(-n // b)
+    fwd = ora.hilbert3d_order((f, h_, w))
+    inv = ora.invert_permutation(fwd)
     dense_layers = set(int(x) for x in t["dense_layers"])
     for step in range(T):
         for layer in range(L):
@@ -356,36 +361,33 @@ def test_trajectory_masks_match_reference(golden):
                 q, k, v = ora.trajectory_at((f, h_, w), d, 4.0, seed, T, 2.0, 0.0, step)
                 Qs.append(q), Ks.append(k), Vs.append(v)
             Q, K, V = (np.stack(x, 1) for x in (Qs, Ks, Vs))
-            # the reference runs fp32; the batched path takes bf16, so the
-            # masks compare on the reference's masks only where inputs agree:
-            # feed bf16-rounded copies to both sides is not possible here, so
-            # compare the *oracle on bf16 inputs* masks instead (bit-exact
-            # given the generic fp64 scorer) and flags against the reference
-            out, st = m.run_step(cu(Q, torch.bfloat16), cu(K, torch.bfloat16), cu(V, torch.bfloat16),
-                                 (f, h_, w), params, sched, cache, layer, step, force_dense=layer in dense_layers)
+            out, st = m.run_step(cu(Q), cu(K), cu(V), (f, h_, w), params, sched, cache, layer, step,
+                                 force_dense=layer in dense_layers)
+            out = host(out)
             for head in range(H):
                 row = step * L * H + layer * H + head
                 flags = int(t["flags"][row])
                 assert st.dense == bool(flags & 1), (step, layer, head)
-                if not st.dense:
-                    assert st.mask_updated[head] == bool(flags & 2), (step, layer, head)
-                    if st.mask_updated[head]:
-                        fwd = ora.hilbert3d_order((f, h_, w))
-                        rq = ora.apply_permutation(fwd, bf16_round(Q[:, head]))
-                        rk = ora.apply_permutation(fwd, bf16_round(K[:, head]))
-                        want = ora.build_mask(rq, rk, b, bs, st.budget)
-                        got, ls = cache.find(layer, head)
-                        assert ls == step
-                        agree = (mask_bits_to_dense(host(got.bits), mm) == mask_bits_to_dense(want, mm)).mean()
-                        assert agree == 1.0, (step, layer, head, agree)
-                        ref_agree = (mask_bits_to_dense(t["masks"][row], mm) == mask_bits_to_dense(want, mm)).mean()
-                        assert ref_agree >= 0.9
+                assert st.budget == t["budget"][row] and st.sparsity[head] == t["sparsity"][row], (step, layer, head)
+                if layer == 0 and head == 0:  # the reference's own output of (layer 0, head 0), every step
+                    assert np.abs(out[:, 0] - t["out00"][step]).max() <= 1e-5, step
+                if st.dense:
+                    continue
+                assert st.mask_updated[head] == bool(flags & 2), (step, layer, head)
+                got, ls = cache.find(layer, head)
+                if st.mask_updated[head]:
+                    assert ls == step
+                    assert (host(got.bits) == t["masks"][row]).all(), (step, layer, head)
+                rq, rk, rv = (ora.apply_permutation(fwd, x[:, head]) for x in (Q, K, V))
+                ref = ora.apply_permutation(inv, ora.block_sparse_attention(rq, rk, rv, host(got.bits), mm, b))
+                assert np.abs(out[:, head] - ref).max() <= 1e-5, (step, layer, head)
 
 
 @pytest.mark.parametrize("d", [96, 128])
 def test_run_step_generic_and_tcgen05_paths(d):
-    """run_step at B = 128 on a ragged lattice: d = 96 takes the geometry-generic kernels
-    (fp64 scorer, SIMT attention with the gathered query rows), d = 128 the tcgen05 ones.
+    """run_step at B = 128 on a ragged lattice: d = 96 is refused by default and, opted in,
+    takes the geometry-generic kernels (fp64 scorer, SIMT attention with the gathered
+    query rows); d = 128 the tcgen05 ones.
     Masks: bit-exact vs the oracle for the fp64 scorer, >= 99.5 % agreement for the
     fp16x3 one; outputs vs the oracle's attention under the device's own mask."""
     m = dfs()
@@ -399,6 +401,11 @@ def test_run_step_generic_and_tcgen05_paths(d):
     sched = m.SparsitySchedule(total_steps=1, warmup_fraction=0.0, phase_budgets=(gam,), phase_fraction=1.0,
                                update_interval=1)
     cache = m.MaskCache()
+    if d == 96:  # outside the tcgen05 contract: refused up front (nothing cached), unless opted in
+        with pytest.raises(m._capi.UnsupportedGeometry):
+            m.run_step(Q, K, V, dims, m.ScoringParams(b, bs), sched, cache, layer=0, step=0)
+        assert cache.size() == 0
+        cache.handle.set_option(2, 1)  # DFS_OPT_GENERIC_ATTN
     out, st = m.run_step(Q, K, V, dims, m.ScoringParams(b, bs), sched, cache, layer=0, step=0)
     out = host(out.float())
     fwd = ora.hilbert3d_order(dims)
@@ -415,3 +422,36 @@ def test_run_step_generic_and_tcgen05_paths(d):
             assert (got == want).mean() >= 0.995
         ref = ora.apply_permutation(inv, ora.block_sparse_attention(rq, rk, rv, bits, mm, b))
         assert _rel_err(out[:, h], ref) <= 2e-2, (d, h)
+
+
+@pytest.mark.parametrize("which", ["q", "k", "v"])
+def test_run_step_nonfinite_refused_by_default(which):
+    """attention.cpp:19-20: non-finite input is an error — by default, on update, reuse and
+    dense steps; the step raises before anything is scored or cached, so a NaN step leaves
+    the previous mask (and its update step) in place."""
+    m = dfs()
+    dims, H, d, b, bs = (4, 16, 32), 2, 128, 128, 16
+    n = int(np.prod(dims))
+    g = torch.Generator().manual_seed(3)
+    q, k, v = (torch.randn(n, H, d, generator=g).to(torch.bfloat16).cuda() for _ in range(3))
+    sched = m.SparsitySchedule(total_steps=4, warmup_fraction=0.25, phase_budgets=(0.25,), phase_fraction=0.75,
+                               update_interval=2)
+    params = m.ScoringParams(b, bs)
+    cache = m.MaskCache()
+    bad = {"q": q, "k": k, "v": v}
+    t = bad[which].clone()
+    t[n // 2, 1, 5] = float("nan")
+    bad[which] = t
+    with pytest.raises(ValueError):  # dense step
+        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 0)
+    with pytest.raises(ValueError):  # first sparse step: nothing cached
+        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 1)
+    assert cache.size() == 0
+    m.run_step(q, k, v, dims, params, sched, cache, 0, 1)
+    before = [cache.find(0, h)[0].bits.clone() for h in range(H)]
+    for step in (2, 3):  # reuse step, then an update step: refused, cache untouched
+        with pytest.raises(ValueError):
+            m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, step)
+        for h in range(H):
+            found = cache.find(0, h)
+            assert found[1] == 1 and torch.equal(found[0].bits, before[h])

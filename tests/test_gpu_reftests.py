@@ -84,3 +84,48 @@ def test_cmd_run_outputs_byte_identical_to_reference(name, tmp_path):
     assert ref_masks and ref_masks == sorted(p.name for p in (gpu / "masks").iterdir())
     for fname in ref_masks:
         assert (ref / "masks" / fname).read_bytes() == (gpu / "masks" / fname).read_bytes(), fname
+
+
+def test_cmd_gpu_runs_the_north_star_shape(tmp_path):
+    """The reference's own cmd_run (commands.cpp:221-319) driving the drop-in library at
+    the HunyuanVideo-720p lattice (118,800 tokens, d = 128, B = 128, B_s = 16, gamma = 0.1)
+    — past the 4096-row cap where the reference's block_scores throws: run_trajectory
+    batches each layer's heads into one device step (fp32 pooling + the fp32-accurate
+    tcgen05 scorer, K5 tcgen05 attention). The DFSM masks it writes must agree with the C
+    oracle's masks on the same fp32 inputs on >= 99.5 % of bits; the
+    report carries the streamed recall (recorded past the cap)."""
+    import json
+
+    import numpy as np
+
+    from oracle import mask_bits_to_dense, ora
+
+    exe = os.path.join(BIN, "cmd_gpu")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built")
+    dims, d, heads = [33, 45, 80], 128, 2
+    cfg = {"seed": 5, "total_steps": 2, "warmup_fraction": 0.5, "phase_budgets": [0.1], "phase_fraction": 0.5,
+           "update_interval": 1, "ordering": "hilbert3d", "block_size": 128, "sub_block_size": 16, "dims": dims,
+           "head_dim": d, "layers": 1, "heads": heads,
+           "trajectory": {"smoothness": 4, "noise_start": 0.5, "noise_end": 0.0}}
+    (tmp_path / "run.json").write_text(json.dumps(cfg))
+    out = tmp_path / "out"
+    r = subprocess.run([exe, "run", str(tmp_path / "run.json"), str(out), str(os.cpu_count() or 4)],
+                       capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+    rows = (out / "report.csv").read_text().strip().splitlines()
+    assert len(rows) == 1 + 2 * heads
+    n = dims[0] * dims[1] * dims[2]
+    m = -(-n // 128)
+    k = ora.topk_count(0.1, m)
+    fwd = ora.hilbert3d_order(dims)
+    for head in range(heads):
+        raw = (out / "masks" / f"mask_step001_layer00_head{head:02d}.dfsm").read_bytes()
+        assert raw[:4] == b"DFSM" and int.from_bytes(raw[8:12], "little") == m
+        got = mask_bits_to_dense(np.frombuffer(raw[16:], np.uint8), m)
+        assert (got.sum(1) == k).all()
+        seed = ora.derive_seed(5, [head])
+        q, kk, _ = ora.trajectory_at(dims, d, 4.0, seed, 2, 0.5, 0.0, 1)
+        want = mask_bits_to_dense(ora.build_mask(ora.apply_permutation(fwd, q), ora.apply_permutation(fwd, kk),
+                                                 128, 16, 0.1), m)
+        assert (got == want).mean() >= 0.995, head
