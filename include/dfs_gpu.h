@@ -248,11 +248,13 @@ typedef struct {
   int layer;
   int step;
   int force_dense;
-  /* Non-finite input is an error (attention.cpp:19-20): the step ORs a device flag
-   * in the passes that read q/k/v anyway (K2, or a check pass on dense / reuse
-   * steps), reads it back once before it scores or touches the mask cache, and
-   * returns DFS_E_INVALID with the cache and output untouched. `nonfinite`
-   * optionally names the device flag to use (caller-zeroed); NULL = the handle's. */
+  /* Non-finite input is an error (attention.cpp:19-20), in the reference's order:
+   * flags are ORed in the passes that read q/k/v anyway (K2, or a check pass on dense
+   * / reuse steps); a non-finite q or k returns DFS_E_INVALID before anything is
+   * scored or cached (build_mask -> attention_scores throws), a non-finite v after
+   * the new masks are stored (block_sparse_attention throws after cache.store,
+   * scheduler.cpp:113-122); no output is written in either case. `nonfinite`
+   * optionally names the device flag for q/k (caller-zeroed); NULL = the handle's. */
   int32_t* nonfinite;
   /* outputs (host, optional) */
   int* dense_out;        /* 1 if the step ran dense */

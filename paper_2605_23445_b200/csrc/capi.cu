@@ -157,6 +157,21 @@ struct dfs_handle {
   Buf q16, k16, v16, o16;                // DFS_F32 steps past the compatibility cap: bf16 copies
   Buf f32_q, f32_k, f32_v, probs, bits;  // DFS_F32 compatibility steps: reordered fp32 [H, N, d]
   Buf peer_tabs;                         // Ulysses: q/k/v/o dfs_peer_table on the device
+  // side stream for the V reorder (only K5 needs it: it runs under K3/K4) + its events
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_v = nullptr;
+  ~dfs_handle() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_v) cudaEventDestroy(ev_v);
+    if (aux) cudaStreamDestroy(aux);
+  }
+  int ensure_aux() {
+    if (aux) return DFS_OK;
+    DFS_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    DFS_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    DFS_CUDA_CHECK(cudaEventCreateWithFlags(&ev_v, cudaEventDisableTiming));
+    return DFS_OK;
+  }
   int64_t total_bytes() const {
     int64_t t = 0;
     for (const Buf* b : {&scratch_i32, &flag, &k_hnd, &v_hnd, &pooled_q, &pooled_k, &scores, &score_ws,
@@ -933,11 +948,16 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
   const int64_t m = ceil_div(n, B);
   int rc;
   int32_t* flag = a->nonfinite;
+  if ((rc = h->step_flag.ensure(2 * sizeof(int32_t)))) return rc;
+  int32_t* flag_v = h->step_flag.as<int32_t>() + 1;  // V's, when its reorder runs on the side stream
   if (!flag) {
-    if ((rc = h->step_flag.ensure(sizeof(int32_t)))) return rc;
     flag = h->step_flag.as<int32_t>();
-    DFS_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int32_t), s));
+    DFS_CUDA_CHECK(cudaMemsetAsync(flag, 0, 2 * sizeof(int32_t), s));
+  } else {
+    DFS_CUDA_CHECK(cudaMemsetAsync(flag_v, 0, sizeof(int32_t), s));
   }
+  bool v_aside = false;  // V reordered on h->aux (joined before K5)
+  bool v_late = false;   // V's finite flag (flag_v) is checked after the mask commit
   // q or k through the prologue: raster -> dst (reordered by idx, or raster for idx == NULL)
   auto prologue = [&](const void* x, void* dst, int layout, const uint32_t* idx, float* pooled, const float* w) {
     return prologue_permute_impl(x, dst, layout, idx, n, H, d, pooled, Bs, flag, w, pro->eps, pro->rope_layout,
@@ -1041,9 +1061,10 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
                                 flag, false, s)) ||
         (rc = permute_rows_impl(a->k, DFS_NHD, h->f32_k.p, DFS_HND, DFS_F32, fwd, n, H, d, pk, update_any ? Bs : 1,
                                 flag, false, s)) ||
-        (rc = permute_rows_impl(a->v, DFS_NHD, h->f32_v.p, DFS_HND, DFS_F32, fwd, n, H, dv, nullptr, 1, flag, false,
+        (rc = permute_rows_impl(a->v, DFS_NHD, h->f32_v.p, DFS_HND, DFS_F32, fwd, n, H, dv, nullptr, 1, flag_v, false,
                                 s)))
       return rc;
+    v_late = true;
     att_q = h->f32_q.p;
     att_k = h->f32_k.p;
     att_v = h->f32_v.p;
@@ -1085,11 +1106,24 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     } else if (dtype == DFS_BF16 && (rc = finite_check_impl(q, n * H * d, DFS_BF16, flag, s))) {
       return rc;
     }
-    if (!pro && ((rc = permute_rows_impl(k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, pk ? Bs : 1,
-                                         flag, false, s)) ||
-                 (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag,
-                                         false, s))))
+    if (!pro && (rc = permute_rows_impl(k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, pk ? Bs : 1,
+                                        flag, false, s)))
       return rc;
+    if (!pro && dtype == DFS_BF16) {
+      // V's reordered copy is read only by K5: on an update step it runs on the side stream
+      // under the flag read-back and K3/K4 (compute-bound), off the critical path
+      if ((rc = h->ensure_aux())) return rc;
+      DFS_CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+      DFS_CUDA_CHECK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+      if ((rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag_v, false,
+                                  h->aux)))
+        return rc;
+      DFS_CUDA_CHECK(cudaEventRecord(h->ev_v, h->aux));
+      v_aside = v_late = true;
+    } else if (!pro && (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1,
+                                               flag, false, s))) {
+      return rc;
+    }
   }
   if ((rc = check_flag(flag, s))) return rc;  // nothing scored, cached or written yet
 
@@ -1097,6 +1131,12 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
                                              h->pooled_q.as<float>(), h->pooled_k.as<float>(), &L, s)))
     return rc;
 
+  if (v_late) {
+    // V is checked like the reference's block_sparse_attention checks it: after build_mask
+    // stored the mask (scheduler.cpp:113-122), before any output is produced
+    if ((rc = check_flag(flag_v, v_aside ? h->aux : s))) return rc;
+    if (v_aside) DFS_CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_v, 0));
+  }
   // attention over the selected blocks; output row i -> raster row fwd[i] (scheduler.cpp:134)
   if (compat) {
     rc = attn_simple(h, att_q, att_k, att_v, a->o, DFS_F32, DFS_HND, nullptr, DFS_NHD, fwd, H, n, d, dv, B,

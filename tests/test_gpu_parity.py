@@ -426,9 +426,10 @@ def test_run_step_generic_and_tcgen05_paths(d):
 
 @pytest.mark.parametrize("which", ["q", "k", "v"])
 def test_run_step_nonfinite_refused_by_default(which):
-    """attention.cpp:19-20: non-finite input is an error — by default, on update, reuse and
-    dense steps; the step raises before anything is scored or cached, so a NaN step leaves
-    the previous mask (and its update step) in place."""
+    """attention.cpp:19-20: non-finite input is an error — by default, on dense, update and
+    reuse steps — with the reference's ordering: a non-finite q or k raises from build_mask
+    (attention_scores) before the mask is stored, a non-finite v from block_sparse_attention
+    AFTER build_mask stored it (scheduler.cpp:113-122); no output is written either way."""
     m = dfs()
     dims, H, d, b, bs = (4, 16, 32), 2, 128, 128, 16
     n = int(np.prod(dims))
@@ -442,16 +443,21 @@ def test_run_step_nonfinite_refused_by_default(which):
     t = bad[which].clone()
     t[n // 2, 1, 5] = float("nan")
     bad[which] = t
+    out = torch.zeros_like(q)
     with pytest.raises(ValueError):  # dense step
-        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 0)
-    with pytest.raises(ValueError):  # first sparse step: nothing cached
-        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 1)
-    assert cache.size() == 0
+        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 0, out=out)
+    with pytest.raises(ValueError):  # first sparse step: nothing cached yet
+        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 1, out=out)
+    assert cache.size() == (H if which == "v" else 0)
+    assert not out.any()  # no output written
     m.run_step(q, k, v, dims, params, sched, cache, 0, 1)
     before = [cache.find(0, h)[0].bits.clone() for h in range(H)]
-    for step in (2, 3):  # reuse step, then an update step: refused, cache untouched
-        with pytest.raises(ValueError):
-            m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, step)
-        for h in range(H):
-            found = cache.find(0, h)
-            assert found[1] == 1 and torch.equal(found[0].bits, before[h])
+    with pytest.raises(ValueError):  # reuse step
+        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 2, out=out)
+    for h in range(H):
+        assert cache.find(0, h)[1] == 1 and torch.equal(cache.find(0, h)[0].bits, before[h])
+    with pytest.raises(ValueError):  # update step: only a bad v lets the new mask be stored
+        m.run_step(bad["q"], bad["k"], bad["v"], dims, params, sched, cache, 0, 3, out=out)
+    for h in range(H):
+        assert cache.find(0, h)[1] == (3 if which == "v" else 1)
+    assert not out.any()
