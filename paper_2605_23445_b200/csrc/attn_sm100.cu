@@ -54,6 +54,16 @@ constexpr uint32_t kTmemCols = 512;
 #endif
 constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
 constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-row group (0 = __syncthreads)
+// d = 64: the two softmax warpgroups run DECOUPLED (no per-block row-max exchange): each
+// keeps its own running max / sum for its 64 key columns and its own O accumulator in
+// TMEM (O_0 at column 384, O_1 at 448: 3 S buffers + 2 x 64 columns = 512), PV_j is two
+// K = 64 MMAs (P_0 V[0:64] -> O_0, P_1 V[64:128] -> O_1) gated by per-warpgroup barriers,
+// and the two partial rows are merged once per tile in the epilogue,
+// O = (2^(m0-m) O_0 + 2^(m1-m) O_1) / (2^(m0-m) l_0 + 2^(m1-m) l_1). At d = 128 TMEM has
+// no room for a second O next to three S buffers, so d = 128 keeps the exchange.
+#ifndef DFS_ATTN_SPLIT_O_D64
+#define DFS_ATTN_SPLIT_O_D64 1
+#endif
 
 template <int D>
 struct Cfg {
@@ -95,6 +105,7 @@ struct Bars {
   uint64_t p_full[3], o_done[3];  // per S/P buffer: the softmax may run a block ahead of PV
   uint64_t kv_full[12], kv_empty[12];
   uint32_t tmem_base;
+  uint64_t p_full1[3];  // decoupled d = 64: warpgroup 1's P of each buffer (p_full: warpgroup 0's)
 };
 
 // (begin, count) of a tile's key-block list, loaded one tile ahead by every role so the
@@ -146,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = Cfg<D>;
+  constexpr bool kSplitO = D == 64 && kWG == 2 && DFS_ATTN_SPLIT_O_D64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offset, so the pointer keeps its shared state space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -160,7 +172,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars->q_empty, 1);
     for (int i = 0; i < 3; ++i) {
       mbar_init(&bars->s_full[i], 1);
-      mbar_init(&bars->p_full[i], kSoftmaxThreads / 32);  // one arrive per softmax warp
+      if constexpr (kSplitO) {  // one arrive per warp of the owning warpgroup
+        mbar_init(&bars->p_full[i], 4);
+        mbar_init(&bars->p_full1[i], 4);
+      } else {
+        mbar_init(&bars->p_full[i], kSoftmaxThreads / 32);  // one arrive per softmax warp
+      }
       mbar_init(&bars->o_done[i], 1);
     }
     for (int i = 0; i < C::kStages; ++i) {
@@ -313,6 +330,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&](bool first) {
       const uint32_t slot = next_slot();
       const uint32_t pb = pv_iter % C::kSBufs;
+      if constexpr (kSplitO) {  // two K = 64 halves, each as soon as its warpgroup's P is in
+        const uint32_t v_lo = ring_lo_v + slot * (C::kTileBytes >> 4);
+        const uint32_t p_tmem = tmem + pb * 128;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(half ? &bars->p_full1[pb] : &bars->p_full[pb], (pv_iter / C::kSBufs) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int s = 4 * half; s < 4 * half + 4; ++s)
+              umma_ts(tmem + C::kOCol + half * D, p_tmem + s * 8, v_lo + ((s * 16 * 128) >> 4), kHiK, C::kIdescPV,
+                      (!first || s > 4 * half) ? 1u : 0u);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          umma_commit(&bars->kv_empty[slot]);
+          umma_commit(&bars->o_done[pb]);
+        }
+        __syncwarp();
+        ++pv_iter;
+        return;
+      }
       trace(p, 2, pv_iter);
       mbar_wait(&bars->p_full[pb], (pv_iter / C::kSBufs) & 1);
       trace(p, 3, pv_iter);
@@ -394,6 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) trace(p, 4 + (wg & 1) * 4, s_iter);
         mbar_wait(&bars->s_full[sb], s_phase);
         if (tr) trace(p, 5 + (wg & 1) * 4, s_iter);
+        // observe every o_done phase once (mbarrier protocol hygiene, compute-sanitizer
+        // synccheck): S_j ready implies PV_{j-3} — the previous phase of this o_done — is
+        // complete (in-order tcgen05 pipe), so this wait returns on its first probe
+        if (threadIdx.x == 64 && s_iter >= C::kSBufs) wait_pv(s_iter - C::kSBufs);
         tc_fence_after();
 #ifdef DFS_ATTN_SKIP_SOFTMAX  // experiment builds only: isolate the MMA/TMA side
         (void)red_par;
@@ -419,11 +463,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < kCPT; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-        red_par[wg * kBM + r] = mx;
-        named_bar_sync(bar_rows, kWG * 32);            // every slice of these rows published its max
-        if (tr) trace(p, 6 + (wg & 1) * 4, s_iter);
+        if constexpr (!kSplitO) {
+          red_par[wg * kBM + r] = mx;
+          named_bar_sync(bar_rows, kWG * 32);            // every slice of these rows published its max
+          if (tr) trace(p, 6 + (wg & 1) * 4, s_iter);
 #pragma unroll
-        for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
+          for (int w = 0; w < kWG; ++w) mx = fmaxf(mx, red_par[w * kBM + r]);
+        }
         const float m_new = fmaxf(m, mx * p.scale_log2);
         // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
         // (the partner warps cover the same rows, so they decide identically)
@@ -437,8 +483,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           lsum[0] = f2_mul(lsum[0], a2);
           lsum[1] = f2_mul(lsum[1], a2);
           m = m_new;
-          const uint32_t o_addr = tmem + lane_addr + C::kOCol + wg * C::kOColsPerWG;
-          if constexpr (C::kOColsPerWG >= 32) {
+          const uint32_t o_addr = tmem + lane_addr + C::kOCol + wg * (kSplitO ? D : C::kOColsPerWG);
+          if constexpr (kSplitO) {  // this warpgroup's own O: all d columns
+#pragma unroll
+            for (int c = 0; c < D; c += 32) {
+              uint32_t ov[32];
+              tmem_ld32(o_addr + c, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st32(o_addr + c, ov);
+            }
+          } else if constexpr (C::kOColsPerWG >= 32) {
 #pragma unroll
             for (int c = 0; c < C::kOColsPerWG; c += 32) {
               uint32_t ov[32];
@@ -458,7 +514,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // p = 2^(s*scale - m); the use_poly<POLY> pairs on the FMA pipe (offloads MUFU)
-        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
+        // (decoupled d = 64: a slice whose keys were all padding so far has m = -inf; its p = 0)
+        const float m_use = kSplitO && m == -INFINITY ? 0.f : m;
+        const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m_use, -m_use);
         uint32_t pk[kCPT / 2];
 #pragma unroll
         for (int i = 0; i < kCPT / 2; ++i) {
@@ -483,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         if (tr) trace(p, 7 + (wg & 1) * 4, s_iter);
         __syncwarp();  // every lane's P store has completed (tcgen05.wait::st above)
-        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+        if (lane == 0) mbar_arrive(kSplitO && wg ? &bars->p_full1[sb] : &bars->p_full[sb]);
         ++s_iter;
       }
       vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;  // lands during the epilogue
@@ -497,18 +555,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       // scatter this slice's columns of the row to its raster slot
       if (cnt > 0) wait_pv(s_iter - 1);
       tc_fence_after();
-      red_sum[wg * kBM + r] = l;   // dedicated slots: the max slots may still be read by peers
-      named_bar_sync(bar_rows, kWG * 32);
       float l_tot = 0.f;
+      float a_w[2] = {1.f, 1.f};  // decoupled d = 64: weights of O_0, O_1 in the merged row
+      if constexpr (kSplitO) {
+        red_max[wg * kBM + r] = m;  // the (stale) max each slice's P and O were computed with
+        red_sum[wg * kBM + r] = l;
+        named_bar_sync(bar_rows, kWG * 32);
+        const float m0 = red_max[r], m1 = red_max[kBM + r];
+        const float mm = fmaxf(m0, m1);
+        a_w[0] = m0 == -INFINITY ? 0.f : ex2(m0 - mm);
+        a_w[1] = m1 == -INFINITY ? 0.f : ex2(m1 - mm);
+        l_tot = a_w[0] * red_sum[r] + a_w[1] * red_sum[kBM + r];
+      } else {
+        red_sum[wg * kBM + r] = l;   // dedicated slots: the max slots may still be read by peers
+        named_bar_sync(bar_rows, kWG * 32);
 #pragma unroll
-      for (int w = 0; w < kWG; ++w) l_tot += red_sum[w * kBM + r];
+        for (int w = 0; w < kWG; ++w) l_tot += red_sum[w * kBM + r];
+      }
       const int64_t i = i_row;
       // an empty key list (possible only through a caller-built CSR; the BlockMask entry
       // points refuse it like attention.cpp:133-136) yields a zero row, never stale TMEM
       const float inv_l = cnt > 0 ? 1.f / l_tot : 0.f;
       constexpr int kOC = C::kOColsPerWG;
       uint32_t ov[kOC];
-      if constexpr (kOC >= 32) {
+      if constexpr (kSplitO) {  // this warpgroup's output columns of both partial rows, merged
+        static_assert(kOC == 32, "decoupled epilogue: 32 output columns per warpgroup");
+        uint32_t o1[32];
+        tmem_ld32(tmem + lane_addr + C::kOCol + wg * kOC, *reinterpret_cast<uint32_t(*)[32]>(ov));
+        tmem_ld32(tmem + lane_addr + C::kOCol + D + wg * kOC, o1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          ov[c] = __float_as_uint(a_w[0] * __uint_as_float(ov[c]) + a_w[1] * __uint_as_float(o1[c]));
+      } else if constexpr (kOC >= 32) {
 #pragma unroll
         for (int c = 0; c < kOC; c += 32)
           tmem_ld32(tmem + lane_addr + C::kOCol + wg * kOC + c, *reinterpret_cast<uint32_t(*)[32]>(ov + c));
@@ -530,7 +609,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
         }
-#pragma unroll
         // 32-byte stores (STG.256): half the store instructions of 16-byte ones; the store
         // issue at the tile boundary is what holds the warps there
         uint32_t w[kOC / 2];
