@@ -339,9 +339,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           if (elect_one()) {
 #pragma unroll
-            for (int s = 4 * half; s < 4 * half + 4; ++s)
-              umma_ts(tmem + C::kOCol + half * D, p_tmem + s * 8, v_lo + ((s * 16 * 128) >> 4), kHiK, C::kIdescPV,
-                      (!first || s > 4 * half) ? 1u : 0u);
+            for (int s = 4 * half; s < 4 * half + 4; ++s)  // P_1 sits in warpgroup 1's own S columns
+              umma_ts(tmem + C::kOCol + half * D, p_tmem + half * 32 + s * 8, v_lo + ((s * 16 * 128) >> 4), kHiK,
+                      C::kIdescPV, (!first || s > 4 * half) ? 1u : 0u);
           }
           __syncwarp();
         }
@@ -434,10 +434,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tr) trace(p, 4 + (wg & 1) * 4, s_iter);
         mbar_wait(&bars->s_full[sb], s_phase);
         if (tr) trace(p, 5 + (wg & 1) * 4, s_iter);
-        // observe every o_done phase once (mbarrier protocol hygiene, compute-sanitizer
-        // synccheck): S_j ready implies PV_{j-3} — the previous phase of this o_done — is
-        // complete (in-order tcgen05 pipe), so this wait returns on its first probe
+#ifdef DFS_SYNCCHECK_BUILD
+        // sanitizer builds only (tools/sanitize.sh): observe every o_done phase once, so
+        // compute-sanitizer synccheck sees no unobserved phase. S_j ready implies PV_{j-3}
+        // — the previous phase of this o_done — completed (in-order tcgen05 pipe), so the
+        // production kernel may leave phases unobserved: its parity waits (rescale,
+        // epilogue) are never more than one phase behind. (Measured: this one extra probe
+        // per block in warp 2 costs ~5 % SM cycles at HY through the row-group barrier.)
         if (threadIdx.x == 64 && s_iter >= C::kSBufs) wait_pv(s_iter - C::kSBufs);
+#endif
         tc_fence_after();
 #ifdef DFS_ATTN_SKIP_SOFTMAX  // experiment builds only: isolate the MMA/TMA side
         (void)red_par;
@@ -532,10 +537,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           lsum[i & 1] = f2_add(lsum[i & 1], f2_pack(p0, p1));
           pk[i] = pack_bf16(p0, p1);
         }
-        // P_j (bf16 pairs) over the first 64 columns of S[sb]: this slice's kCPT keys -> kCPT/2 columns
+        // P_j (bf16 pairs) over the first 64 columns of S[sb]: this slice's kCPT keys -> kCPT/2 columns.
+        // (Decoupled d = 64: there is no exchange barrier proving the partner has loaded its
+        // S columns, so each warpgroup writes P into its OWN S columns: 0-31 and 64-95.)
+        constexpr int kPStride = kSplitO ? kCPT : kCPT / 2;
 #pragma unroll
         for (int c = 0; c < kCPT / 32; ++c)
-          tmem_st16(tmem + lane_addr + sb * 128 + wg * (kCPT / 2) + c * 16,
+          tmem_st16(tmem + lane_addr + sb * 128 + wg * kPStride + c * 16,
                     *reinterpret_cast<const uint32_t(*)[16]>(pk + 16 * c));
         tmem_wait_st();
         tc_fence_before();
@@ -587,6 +595,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c)
           ov[c] = __float_as_uint(a_w[0] * __uint_as_float(ov[c]) + a_w[1] * __uint_as_float(o1[c]));
+        // both warpgroups read both accumulators: neither may let the next tile's first
+        // PV (which only waits for its own warpgroup's P) overwrite them before the other read
+        named_bar_sync(bar_rows, kWG * 32);
       } else if constexpr (kOC >= 32) {
 #pragma unroll
         for (int c = 0; c < kOC; c += 32)
