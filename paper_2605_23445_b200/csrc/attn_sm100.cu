@@ -64,6 +64,26 @@ constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-ro
 #ifndef DFS_ATTN_SPLIT_O_D64
 #define DFS_ATTN_SPLIT_O_D64 1
 #endif
+// d = 128: Q resident in TMEM (QK^T issued with A from TMEM). Shared memory, not the tensor
+// pipe, bounds the MMA side when Q is an smem operand: per 128 x 128 block QK reads Q and K
+// (64 KB), PV reads V (32 KB) and TMA writes K and V (64 KB) — 160 KB at ~128 B/clk/SM is
+// ~1250 cycles against 1024 tensor cycles (tools/mma_bw.cu; the MMA-only isolation build
+// stalls at ~0.8 of peak). With Q copied once per tile into TMEM (tcgen05.cp, 8 x 128x256b)
+// a block moves 128 KB of smem. TMEM then holds two S buffers: S0 [0,128) S1 [128,256),
+// O [256,384), Q double-buffered at [384,448) / [448,512).
+#ifndef DFS_ATTN_QT
+#define DFS_ATTN_QT 1
+#endif
+// d = 128: softmax warps split the tile by ROWS, not key columns. The two warps sharing a TMEM
+// lane quadrant (and an SMSP) own 16 rows each; a row's 128 logits are held by a thread pair
+// (lanes l and l + 16: tcgen05.ld 16x32bx2, key columns 0-63 / 64-127), so the row max is one
+// shuffle and no warp ever waits for another. With the column split both warps of an SMSP
+// met at a per-block max exchange and ran in lockstep, so their serial phases (S wait, TMEM
+// load, max chain, P store) coincided and the scheduler idled; decoupled, the arbiter's
+// priority staggers them and one warp's latency hides under the other's exponentials.
+#ifndef DFS_ATTN_ROWSPLIT
+#define DFS_ATTN_ROWSPLIT 1
+#endif
 
 template <int D>
 struct Cfg {
@@ -78,8 +98,12 @@ struct Cfg {
   static constexpr int kSmem = kBarOff + 512 + 1024;     // barriers + alignment slack
   static constexpr uint32_t kIdescQK = idesc_bf16_f32(kBM, kBN, false, false);
   static constexpr uint32_t kIdescPV = idesc_bf16_f32(kBM, D, false, true);
-  static constexpr int kSBufs = 3;         // TMEM: S0/P0 [0,128) S1/P1 [128,256) S2/P2 [256,384) O [384,384+D)
-  static constexpr uint32_t kOCol = 384;
+  static constexpr bool kQT = D == 128 && DFS_ATTN_QT;  // Q in TMEM (see DFS_ATTN_QT)
+  // TMEM: S0/P0 [0,128) S1/P1 [128,256) S2/P2 [256,384) O [384,384+D); kQT: two S buffers,
+  // O [256,384), Q [384,448) and [448,512)
+  static constexpr int kSBufs = kQT ? 2 : 3;
+  static constexpr uint32_t kOCol = kQT ? 256 : 384;
+  static constexpr uint32_t kQCol = 384;
   static constexpr int kOColsPerWG = D / kWG;
 };
 
@@ -158,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = Cfg<D>;
   constexpr bool kSplitO = D == 64 && kWG == 2 && DFS_ATTN_SPLIT_O_D64;
+  constexpr bool kRowSplit = D == 128 && kWG == 2 && DFS_ATTN_ROWSPLIT;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offset, so the pointer keeps its shared state space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -278,11 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       // consumption order of the MMA warp (QK runs two blocks ahead of PV):
       // K0, K1, K2, V0, K3, V1, ..., K_{n-1}, V_{n-3}, V_{n-2}, V_{n-1}
+      // (two S buffers, kQT: QK_{j+2} follows PV_j: K0, K1, V0, K2, V1, K3, ...)
       if (cnt > 0) load_tile(&tm_k, h, int64_t(blk(0)) * kBN);
       if (cnt > 1) load_tile(&tm_k, h, int64_t(blk(1)) * kBN);
       for (int32_t j = 0; j < cnt; ++j) {
-        if (j + 2 < cnt) load_tile(&tm_k, h, int64_t(blk(j + 2)) * kBN);
-        load_tile(&tm_v, h, int64_t(blk(j)) * kBN);
+        if constexpr (C::kQT) {
+          load_tile(&tm_v, h, int64_t(blk(j)) * kBN);
+          if (j + 2 < cnt) load_tile(&tm_k, h, int64_t(blk(j + 2)) * kBN);
+        } else {
+          if (j + 2 < cnt) load_tile(&tm_k, h, int64_t(blk(j + 2)) * kBN);
+          load_tile(&tm_v, h, int64_t(blk(j)) * kBN);
+        }
       }
     }
   } else if (warp == 1) {
@@ -308,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Three S/P buffers: QK_{j+2} overwrites S[(j+2)%3], whose P_{j-1} was consumed by
     // PV_{j-1}, issued earlier into the in-order tcgen05 pipe — so QK never waits for the
     // softmax, and the tensor pipe always has the next QK queued behind each PV.
+    uint32_t q_tm = tmem + C::kQCol;  // kQT: this tile's Q buffer in TMEM
     auto issue_qk = [&]() {
       const uint32_t slot = next_slot();
       const uint32_t sb = s_iter % C::kSBufs;
@@ -318,7 +350,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < D / 16; ++s) {
           const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
 #ifndef DFS_ATTN_SKIP_MMA  // experiment builds only (tools/attn_exp.sh): isolate the softmax side
-          umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off, kHiK, C::kIdescQK, s > 0);
+          if constexpr (C::kQT)
+            umma_ts(tmem + sb * 128, q_tm + s * 8, k_lo + off, kHiK, C::kIdescQK, s > 0);
+          else
+            umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off, kHiK, C::kIdescQK, s > 0);
 #endif
         }
         umma_commit(&bars->kv_empty[slot]);
@@ -379,19 +414,204 @@ __global__ void __launch_bounds__(kThreads, 1)
       nxt = load_meta(p, tile + gridDim.x);
       mbar_wait(&bars->q_full, q_phase);
       q_phase ^= 1;
-      if (cnt > 0) issue_qk();
-      if (cnt > 1) issue_qk();
-      auto release_q = [&]() {  // Q smem free once the last QK read it
+      auto release_q = [&]() {  // Q smem free once the last QK read it (kQT: once copied to TMEM)
         if (elect_one()) umma_commit(&bars->q_empty);
         __syncwarp();
       };
-      if (cnt <= 2) release_q();
-      for (int32_t j = 0; j < cnt; ++j) {
-        if (j + 2 < cnt) {
-          issue_qk();
-          if (j + 3 == cnt) release_q();
+      if constexpr (C::kQT) {
+        // Q -> TMEM buffer (tile parity): one 128x256b copy per K step, the same SW128
+        // K-major descriptors the SS MMA used. tcgen05.cp and tcgen05.mma execute in issue
+        // order, and the buffer's previous user (two tiles back) issued all its QKs before.
+        q_tm = tmem + C::kQCol + (q_phase ? 0u : 64u);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int s = 0; s < D / 16; ++s) {
+            const uint32_t off = ((s >> 2) * C::kChunkBytes + (s & 3) * 32) >> 4;
+            tmem_cp_128x256b(q_tm + s * 8, (uint64_t(kHiK) << 32) | (q_lo + off));
+          }
         }
-        issue_pv(j == 0);
+        __syncwarp();
+        release_q();
+        if (cnt > 0) issue_qk();
+        if (cnt > 1) issue_qk();
+        for (int32_t j = 0; j < cnt; ++j) {
+          issue_pv(j == 0);
+          if (j + 2 < cnt) issue_qk();
+        }
+      } else {
+        if (cnt > 0) issue_qk();
+        if (cnt > 1) issue_qk();
+        if (cnt <= 2) release_q();
+        for (int32_t j = 0; j < cnt; ++j) {
+          if (j + 2 < cnt) {
+            issue_qk();
+            if (j + 3 == cnt) release_q();
+          }
+          issue_pv(j == 0);
+        }
+      }
+    }
+  } else if constexpr (kRowSplit) {
+    // ======================= softmax / epilogue, row split (d = 128) ====================
+    // warp w: TMEM lane quadrant w & 3, row half (w - 2) >> 2: rows 32 (w & 3) + 16 half + [0, 16).
+    // Lane l: row (l & 15) of those, key columns 64 (l >> 4) + [0, 64) of every block.
+    const int hf = (warp - 2) >> 2, ch = lane >> 4;
+    const int r = (warp & 3) * 32 + hf * 16 + (lane & 15);  // query row within the tile == TMEM lane
+    const uint32_t lane_addr = uint32_t((warp & 3) * 32 + hf * 16) << 16;
+    uint32_t s_iter = 0;
+    auto wait_pv = [&](uint32_t g) { mbar_wait(&bars->o_done[g % C::kSBufs], (g / C::kSBufs) & 1); };
+    TileMeta nxt = load_meta(p, blockIdx.x);
+    int32_t vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
+    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      const int64_t h = tile / p.mq, u = tile % p.mq;
+      const int32_t beg = nxt.beg, cnt = nxt.cnt;
+      nxt = load_meta(p, tile + gridDim.x);
+      const int64_t i_row = u * kBM + r;
+      const int64_t orow = i_row < p.nq && p.out_rows ? int64_t(__ldg(p.out_rows + i_row)) : i_row;
+      float m = -INFINITY;
+      uint64_t lsum[2] = {0, 0};
+      int32_t vb_next = vb_first;
+      for (int32_t j = 0; j < cnt; ++j) {
+        const int32_t vb = vb_next;
+        if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);
+        const uint32_t sb = s_iter % C::kSBufs;
+        const bool tr = threadIdx.x == 64 || threadIdx.x == 192;
+        if (tr) trace(p, 4 + hf * 4, s_iter);
+        mbar_wait(&bars->s_full[sb], (s_iter / C::kSBufs) & 1);
+        if (tr) trace(p, 5 + hf * 4, s_iter);
+#ifdef DFS_SYNCCHECK_BUILD
+        if (threadIdx.x == 64 && s_iter >= C::kSBufs) wait_pv(s_iter - C::kSBufs);
+#endif
+        tc_fence_after();
+        uint32_t sv[64];
+        const int valid = int(min(int64_t(kBN), p.nk - int64_t(vb) * kBN)) - ch * 64;
+        auto load_s = [&]() {
+          tmem_ld16x2_x64<64>(tmem + lane_addr + sb * 128, sv);
+          tmem_wait_ld();
+          if (valid < 64) {  // padded keys of a partial last block (attention.cpp:146-152)
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+              if (i >= valid) sv[i] = __float_as_uint(-INFINITY);
+          }
+        };
+        load_s();
+        if (tr && hf == 0) trace(p, 12, s_iter);
+        // The running max m is stale by design (O is rescaled only when a block raises it by
+        // more than kRescaleThreshold), so the exponentials of block j need only m, not block
+        // j's own max: they start right after the TMEM load, and the threshold test runs on
+        // their arguments x = s * scale - m (max(x) > threshold), reduced on the ALU pipe inside
+        // the same loop — off the critical path. A block that crosses it (rare: ~0.03 % of
+        // blocks at HY) rescales O and recomputes its exponentials before P is stored. The
+        // first block of a tile sets m from its own max.
+        if (j == 0) {
+          float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int i = 0; i < 64; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
+          const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+          m = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * p.scale_log2;  // + the row's other 64 keys
+        }
+        uint32_t pk[32];
+        uint64_t lb[2];
+        float xmax;
+        auto exps = [&]() {
+          const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
+          lb[0] = lb[1] = 0;
+          float xm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float x0, x1;
+            f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
+            xm[i & 3] = fmaxf(xm[i & 3], fmaxf(x0, x1));
+            float p0, p1;
+            if (use_poly<POLY>(i)) {
+              f2_unpack(ex2_poly2(x0, x1), p0, p1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            lb[i & 1] = f2_add(lb[i & 1], f2_pack(p0, p1));
+            pk[i] = pack_bf16(p0, p1);
+          }
+          xmax = fmaxf(fmaxf(xm[0], xm[1]), fmaxf(xm[2], xm[3]));
+        };
+        exps();
+        if (j > 0) {
+          xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, 16));  // the row's other 64 keys
+          if (__any_sync(0xffffffffu, xmax > kRescaleThreshold)) {  // warp-uniform (TMEM ops below)
+            const float m_new = m + fmaxf(xmax, 0.f);
+            wait_pv(s_iter - 1);  // PV_{j-1} complete: O stable
+            tc_fence_after();
+            const float alpha = ex2(m - m_new);
+            const uint64_t a2 = f2_pack(alpha, alpha);
+            lsum[0] = f2_mul(lsum[0], a2);
+            lsum[1] = f2_mul(lsum[1], a2);
+            m = m_new;
+#pragma unroll
+            for (int c = 0; c < D / 2; c += 32) {  // this thread's D/2 output columns of the row
+              uint32_t ov[32];
+              tmem_ld16x2_x32<D / 2>(tmem + lane_addr + C::kOCol + c, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st16x2_x32<D / 2>(tmem + lane_addr + C::kOCol + c, ov);
+            }
+            load_s();  // S_j is still in TMEM (P not yet stored): reload instead of keeping sv live
+            exps();
+          }
+        }
+        lsum[0] = f2_add(lsum[0], lb[0]);
+        lsum[1] = f2_add(lsum[1], lb[1]);
+        if (tr && hf == 0) trace(p, 14, s_iter);
+        // P_j (bf16 pairs) over S columns 0-63 of the row: keys 64 ch + [0, 64) -> columns 32 ch + [0, 32)
+        tmem_st16x2_x32<32>(tmem + lane_addr + sb * 128, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        if (tr) trace(p, 7 + hf * 4, s_iter);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+        ++s_iter;
+      }
+      vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
+      float l;
+      {
+        float a, b;
+        f2_unpack(f2_add(lsum[0], lsum[1]), a, b);
+        l = a + b;
+      }
+      l += __shfl_xor_sync(0xffffffffu, l, 16);
+      if (cnt > 0) wait_pv(s_iter - 1);
+      tc_fence_after();
+      const float inv_l = cnt > 0 ? 1.f / l : 0.f;
+      uint32_t ov[D / 2];
+      tmem_ld16x2_x64<D / 2>(tmem + lane_addr + C::kOCol, ov);
+      tmem_wait_ld();
+      tc_fence_before();
+      if (i_row < p.nq) {
+        __nv_bfloat16* dst;
+        if constexpr (kPeerOut) {
+          const int64_t nl = p.out_peers->n_local, rk = orow / nl;
+          dst = static_cast<__nv_bfloat16*>(const_cast<void*>(p.out_peers->ptr[rk])) +
+                ((orow - rk * nl) * p.out_peers->heads_total + p.out_peers->h0 + h) * D + ch * (D / 2);
+        } else {
+          dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + ch * (D / 2);
+        }
+        uint32_t w[D / 4];
+#pragma unroll
+        for (int c = 0; c < D / 4; ++c)
+          w[c] = pack_bf16(__uint_as_float(ov[2 * c]) * inv_l, __uint_as_float(ov[2 * c + 1]) * inv_l);
+        if (!kPeerOut && p.out_v8) {
+#pragma unroll
+          for (int q = 0; q < D / 32; ++q)
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst + q * 16),
+                         "r"(w[8 * q + 0]), "r"(w[8 * q + 1]), "r"(w[8 * q + 2]), "r"(w[8 * q + 3]),
+                         "r"(w[8 * q + 4]), "r"(w[8 * q + 5]), "r"(w[8 * q + 6]), "r"(w[8 * q + 7])
+                         : "memory");
+        } else {
+#pragma unroll
+          for (int q = 0; q < D / 16; ++q)
+            *reinterpret_cast<uint4*>(dst + q * 8) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+        }
       }
     }
   } else {
@@ -457,6 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kCPT / 32; ++c)
           tmem_ld32(tmem + lane_addr + sb * 128 + wg * kCPT + c * 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * c));
         tmem_wait_ld();
+        if (tr && wg == 0) trace(p, 12, s_iter);
         // padded keys of a partial last block (attention.cpp:146-152); warp-uniform branch
         const int valid = int(min(int64_t(kBN), p.nk - int64_t(vb) * kBN)) - wg * kCPT;
         if (valid < kCPT) {
@@ -468,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < kCPT; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
         float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        if (tr && wg == 0) trace(p, 13, s_iter);
         if constexpr (!kSplitO) {
           red_par[wg * kBM + r] = mx;
           named_bar_sync(bar_rows, kWG * 32);            // every slice of these rows published its max
@@ -537,6 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           lsum[i & 1] = f2_add(lsum[i & 1], f2_pack(p0, p1));
           pk[i] = pack_bf16(p0, p1);
         }
+        if (tr && wg == 0) trace(p, 14, s_iter);
         // P_j (bf16 pairs) over the first 64 columns of S[sb]: this slice's kCPT keys -> kCPT/2 columns.
         // (Decoupled d = 64: there is no exchange barrier proving the partner has loaded its
         // S columns, so each warpgroup writes P into its OWN S columns: 0-31 and 64-95.)
@@ -766,8 +989,8 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   p.trace = nullptr;
 #ifdef DFS_ATTN_TRACE_BUILD
   const char* trace_path = getenv("DFS_ATTN_TRACE");
-  if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 16 * 256 * sizeof(unsigned long long)));
-  if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 16 * 256 * sizeof(unsigned long long), stream));
+  if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 24 * 256 * sizeof(unsigned long long)));
+  if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 24 * 256 * sizeof(unsigned long long), stream));
 #endif
   static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly<D>;
   if (a.out_peers) {  // Ulysses: the epilogue stores into the token owners' shards
@@ -784,7 +1007,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   if (rc) return rc;
 #ifdef DFS_ATTN_TRACE_BUILD
   if (p.trace) {
-    unsigned long long host[16 * 256];
+    unsigned long long host[24 * 256];
     DFS_CUDA_CHECK(cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream));
     DFS_CUDA_CHECK(cudaStreamSynchronize(stream));
     if (FILE* f = fopen(trace_path, "wb")) {

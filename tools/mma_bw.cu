@@ -37,6 +37,21 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int iters, unsigned long lo
   if (threadIdx.x == 0) {
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+      if (mode == 12) {  // mode 10 with Q resident in TMEM (QK as TS: A = Q from TMEM cols 256..319), 2 S buffers
+        const uint32_t sq = ((it + 2) % 2) * 128, sp = (it % 2) * 128;
+        const uint32_t ring = a + 32768;
+        const uint32_t kslot = ring + uint32_t((2 * it) % 5) * 32768, vslot = ring + uint32_t((2 * it + 1) % 5) * 32768;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const uint32_t off = (s >> 2) * 16384 + (s & 3) * 32;
+          umma_f16_ts(tmem + sq, tmem + 256 + s * 8, smem_desc_sw128(kslot + off, 16, 1024), idesc, s > 0);
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          umma_f16_ts(tmem + 384, tmem + sp + s * 8, smem_desc_sw128(vslot + s * 16 * 128, 16384, 1024),
+                      idesc_bf16_f32(128, n_dim, false, true), 1);
+        continue;
+      }
       if (mode == 10 || mode == 11) {  // mode 8's order with K/V operands rotating through 5 ring slots of 32 KB
         const uint32_t sq = ((it + 2) % 3) * 128, sp = (it % 3) * 128;
         const uint32_t ring = a + 32768;  // Q at a (32 KB), ring after it
@@ -178,7 +193,8 @@ KFn pick(int mode, int n) {
     case 8: return pick_n<8>(n);
     case 9: return pick_n<9>(n);
     case 10: return pick_n<10>(n);
-    default: return pick_n<11>(n);
+    case 11: return pick_n<11>(n);
+    default: return pick_n<12>(n);
   }
 }
 
@@ -201,9 +217,11 @@ int main() {
   cudaMalloc(&d, 148 * sizeof(unsigned long long));
   const int smem = 32768 * 6 + 1024;
   const int iters = 4000;
-  for (int mode = 0; mode < 12; ++mode)
+  for (int mode = 0; mode < 13; ++mode)
     for (int n : {64, 128, 256})
-      for (int tma : {0, 4000, 8000}) {
+      for (int tma : {0, 4000, 8000, 16000}) {
+        if (mode == 11 && tma) continue;  // its commits share tbar with the TMA stream
+        if (tma == 16000 && mode < 10) continue;
         if (n == 256 && mode >= 2 && mode < 5) continue;
         if (n == 256 && mode >= 5) continue;
         if (tma && !(mode >= 7 || mode == 0) ) continue;
@@ -223,7 +241,7 @@ int main() {
         unsigned long long c[148];
         cudaMemcpy(c, d, sizeof(c), cudaMemcpyDeviceToHost);
         const double flops = 2.0 * 128 * n * 16 * 8.0 * iters * 148 * (mode >= 7 ? 2 : 1);
-        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8", "TS-MNmajorB", "SS-MNmajorB", "K5:SS8,TS8(P=S)", "3buf:QK(j+2),PV(j)", "3buf:PV(j),QK(j+2)", "3buf+5 ring slots", "3buf+ring+commits"}[mode], n, tma,
+        printf("%s N=%d tma_tiles=%d: %.1f cyc/MMA (clk64), %.3f ms, %.0f TFLOP/s  err=%s\n", (const char*[]){"SS", "TS", "SSx2", "SS+TS", "SS8+TS8", "TS-MNmajorB", "SS-MNmajorB", "K5:SS8,TS8(P=S)", "3buf:QK(j+2),PV(j)", "3buf:PV(j),QK(j+2)", "3buf+5 ring slots", "3buf+ring+commits", "Q-in-TMEM(TS QK)+ring"}[mode], n, tma,
                double(c[0]) / (iters * 8 * (mode >= 7 ? 2 : 1)), ms, flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
