@@ -6,15 +6,17 @@
 // (top-K LUT, or every block for dense / cross attention), so masked blocks
 // cost neither bytes nor FLOPs.
 //
-// Warp roles (64 + 128 * kWG threads; kWG = 2 -> 320):
+// Warp roles (128 * kWG + 64 threads; kWG = 2 -> 320). The MMA issuer takes the HIGHEST warp
+// id: the SMSP arbiter issues highest-id first, and the issuer shares its SMSP with two
+// softmax warps — at the lowest id it saw P_j ~500 cycles late and was as slow to issue PV_j.
 //   warp 0      TMA producer: Q tile (TMA tile::gather4 of raster rows when the
 //               reorder is fused), then K_0, K_1, K_2, V_0, K_3, V_1, ... into a
 //               ring of kStages smem slots (SWIZZLE_128B boxes of 128 x 64).
-//   warp 1      MMA issuer (one elected lane): S_j = Q K_j^T into one of three
+//   warp 9      MMA issuer (one elected lane): S_j = Q K_j^T into one of three
 //               TMEM S buffers (QK runs two blocks ahead of PV, so the tensor pipe
 //               always has work queued behind each PV), then O += P_j V_j with P_j
 //               read straight from TMEM (bf16, aliasing S_j) and O resident in TMEM.
-//   warps 2..   softmax / correction / epilogue: kWG warpgroups split the 128 key
+//   warps 1-8   softmax / correction / epilogue: kWG warpgroups split the 128 key
 //               columns of every query row (TMEM lane); each thread handles
 //               128 / kWG logits per block and the row max is exchanged through
 //               shared memory with one named barrier per block. Online softmax in
@@ -27,6 +29,7 @@
 // are computed on TMA zero-fill and never stored (attention.cpp:146-152).
 #include <cuda.h>
 
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 
@@ -48,6 +51,7 @@ constexpr int kWG = DFS_ATTN_WG;           // softmax warpgroups splitting the 1
 constexpr int kCPT = 128 / kWG;            // key columns (logits) per softmax thread per block
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
+constexpr int kMmaWarp = kSoftmaxThreads / 32 + 1;  // 9; softmax warps 1 .. kSoftmaxThreads / 32
 constexpr uint32_t kTmemCols = 512;
 #ifndef DFS_ATTN_RESCALE_LOG2
 #define DFS_ATTN_RESCALE_LOG2 8.0f
@@ -151,6 +155,9 @@ __device__ __forceinline__ TileMeta load_meta(const Params& p, int64_t tile) {
   return t;
 }
 
+#ifndef DFS_TRACE_T0
+#define DFS_TRACE_T0 64  // traced softmax warps: T0 / 32 and T0 / 32 + 4 (one SMSP)
+#endif
 #ifdef DFS_ATTN_TRACE_BUILD
 __device__ __forceinline__ void trace(const Params& p, int ev, uint32_t idx) {
   if (p.trace && blockIdx.x == 0 && idx < 256) p.trace[ev * 256 + idx] = clock64();
@@ -216,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tm_k);
     prefetch_tmap(&tm_v);
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(&bars->tmem_base);
+  if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ================================ MMA issuer ================================
     // Warp-uniform control flow, one elected lane issues. Descriptors are kept as
     // 32-bit halves: per K step only the low word moves (one uniform add), which
@@ -360,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bars->s_full[sb]);
       }
       __syncwarp();
+      trace(p, 17, s_iter);
       ++s_iter;
     };
     auto issue_pv = [&](bool first) {
@@ -406,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma_commit(&bars->o_done[pb]);
       }
       __syncwarp();
+      trace(p, 16, pv_iter);
       ++pv_iter;
     };
     TileMeta nxt = load_meta(p, blockIdx.x);
@@ -456,11 +465,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ======================= softmax / epilogue, row split (d = 128) ====================
     // warp w: TMEM lane quadrant w & 3, row half (w - 2) >> 2: rows 32 (w & 3) + 16 half + [0, 16).
     // Lane l: row (l & 15) of those, key columns 64 (l >> 4) + [0, 64) of every block.
-    const int hf = (warp - 2) >> 2, ch = lane >> 4;
+    const int hf = (warp - 1) >> 2, ch = lane >> 4;
     const int r = (warp & 3) * 32 + hf * 16 + (lane & 15);  // query row within the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32 + hf * 16) << 16;
     uint32_t s_iter = 0;
-    auto wait_pv = [&](uint32_t g) { mbar_wait(&bars->o_done[g % C::kSBufs], (g / C::kSBufs) & 1); };
+    const uint32_t s_full0 = pin_u32(smem_u32(&bars->s_full[0])), p_full0 = s_full0 + 24, o_done0 = s_full0 + 48;
+    static_assert(offsetof(Bars, p_full) == offsetof(Bars, s_full) + 24 && offsetof(Bars, o_done) == offsetof(Bars, s_full) + 48,
+                  "barrier layout");
+    auto wait_pv = [&](uint32_t g) { mbar_wait_a(o_done0 + (g % C::kSBufs) * 8, (g / C::kSBufs) & 1); };
+    const int32_t nk32 = int32_t(p.nk);
     TileMeta nxt = load_meta(p, blockIdx.x);
     int32_t vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
     for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
@@ -476,16 +489,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int32_t vb = vb_next;
         if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);
         const uint32_t sb = s_iter % C::kSBufs;
-        const bool tr = threadIdx.x == 64 || threadIdx.x == 192;
+        const bool tr = threadIdx.x == DFS_TRACE_T0 || threadIdx.x == DFS_TRACE_T0 + 128;
         if (tr) trace(p, 4 + hf * 4, s_iter);
-        mbar_wait(&bars->s_full[sb], (s_iter / C::kSBufs) & 1);
+        mbar_wait_a(s_full0 + sb * 8, (s_iter / C::kSBufs) & 1);
         if (tr) trace(p, 5 + hf * 4, s_iter);
+        if (lane == 0) trace(p, 25 + warp, s_iter);  // 26..33: S_j seen by softmax warp 1..8
 #ifdef DFS_SYNCCHECK_BUILD
         if (threadIdx.x == 64 && s_iter >= C::kSBufs) wait_pv(s_iter - C::kSBufs);
 #endif
         tc_fence_after();
         uint32_t sv[64];
-        const int valid = int(min(int64_t(kBN), p.nk - int64_t(vb) * kBN)) - ch * 64;
+        const int valid = min(kBN, nk32 - vb * kBN) - ch * 64;
         auto load_s = [&]() {
           tmem_ld16x2_x64<64>(tmem + lane_addr + sb * 128, sv);
           tmem_wait_ld();
@@ -569,7 +583,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         if (tr) trace(p, 7 + hf * 4, s_iter);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->p_full[sb]);
+        if (lane == 0) {
+          trace(p, 17 + warp, s_iter);  // 18..25: P_j arrival of softmax warp 1..8
+          mbar_arrive_a(p_full0 + sb * 8);
+        }
         ++s_iter;
       }
       vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
@@ -618,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ============================ softmax / epilogue ============================
     // kWG warpgroups split the 128 key columns of each block (128 / kWG each); a thread
     // owns one query row (TMEM lane) of its 32-column slice.
-    const int wg = (warp - 2) >> 2;                    // key columns [kCPT*wg, kCPT*wg + kCPT)
+    const int wg = (warp - 1) >> 2;                    // key columns [kCPT*wg, kCPT*wg + kCPT)
     const int r = (warp & 3) * 32 + lane;              // query row within the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
     // A row's max / sum exchange involves only the kWG warps holding that row's slices
@@ -867,7 +884,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<kTmemCols>(tmem);
 }
 
 // ---- host ------------------------------------------------------------------------
@@ -989,8 +1006,8 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   p.trace = nullptr;
 #ifdef DFS_ATTN_TRACE_BUILD
   const char* trace_path = getenv("DFS_ATTN_TRACE");
-  if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 24 * 256 * sizeof(unsigned long long)));
-  if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 24 * 256 * sizeof(unsigned long long), stream));
+  if (trace_path) DFS_CUDA_CHECK(cudaMalloc(&p.trace, 40 * 256 * sizeof(unsigned long long)));
+  if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 40 * 256 * sizeof(unsigned long long), stream));
 #endif
   static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly<D>;
   if (a.out_peers) {  // Ulysses: the epilogue stores into the token owners' shards
@@ -1007,7 +1024,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   if (rc) return rc;
 #ifdef DFS_ATTN_TRACE_BUILD
   if (p.trace) {
-    unsigned long long host[24 * 256];
+    unsigned long long host[40 * 256];
     DFS_CUDA_CHECK(cudaMemcpyAsync(host, p.trace, sizeof(host), cudaMemcpyDeviceToHost, stream));
     DFS_CUDA_CHECK(cudaStreamSynchronize(stream));
     if (FILE* f = fopen(trace_path, "wb")) {

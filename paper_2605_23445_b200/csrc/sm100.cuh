@@ -27,17 +27,47 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-// Wait until the phase with parity `parity` has completed.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// Wait until the phase with parity `parity` has completed. The try_wait carries a suspend-time
+// hint (DFS_MBAR_SUSPEND_NS, 0 = none): the waiting warp sleeps until the phase completes instead
+// of re-issuing the probe — spinning control warps otherwise take issue slots from the softmax
+// warps sharing their SMSP.
+#ifndef DFS_MBAR_SUSPEND_NS
+#define DFS_MBAR_SUSPEND_NS 0
+#endif
+__device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
+#if DFS_MBAR_SUSPEND_NS
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t"
+      "}" ::"r"(addr),
+      "r"(parity), "n"(DFS_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t"
       ".reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t"
-      "}" ::"r"(smem_u32(bar)),
+      "}" ::"r"(addr),
       "r"(parity)
       : "memory");
+#endif
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_a(smem_u32(bar), parity); }
+
+// an opaque copy: keeps a loop-invariant value in a register instead of letting the
+// compiler re-derive it (e.g. a shared address through S2R SR_CgaCtaId) inside a hot loop
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
 
 // ---- CTA pairs (cta_group::2) ------------------------------------------------------

@@ -19,40 +19,76 @@ __device__ __forceinline__ bool poly_at(int i) {
   else if constexpr (POLY == 38) return (0x92u >> (i % 8)) & 1u;
   else return i % POLY == POLY - 1;
 }
-template <int POLY, int PACK>
-__global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, long long* clk, float scale) {
-  // K5's softmax data path: per block, S slice TMEM -> registers (2 x32 loads), exp2 of the
-  // 64 logits, packed bf16 P back to TMEM (2 x16 stores), row sum; 2 warps per SMSP.
+// FEAT bits: 16 = column-split TMEM shapes (32x32b: thread = lane, 64 consecutive columns),
+// 32 = cheap threshold test (x max over the polynomial pairs only + block-sum check), 1 = threshold test (x max over the block, shuffle, vote) as K5's row-split loop,
+// 2 = mbarrier protocol (try_wait on an already-completed phase, fence, syncwarp, lane-0
+// arrive), 4 = per-block LUT load + partial-block bound (as K5), 8 = second warpgroup offset
+// by half a block (a dummy pass first)
+template <int POLY, int PACK, int FEAT = 0>
+__global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, long long* clk, float scale, const int* lut) {
   __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bars[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, wg = warp >> 2;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], (1u << 20) - 1);
+    fence_barrier_init();
+  }
   if (warp == 0) tmem_alloc<512>(&tbase);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(&bars[0]);  // phase 0 completes: later waits on parity 0 return at once
+  __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = tbase, lane_addr = uint32_t((warp & 3) * 32) << 16;
+  const uint32_t tmem = tbase, lane_addr = uint32_t((warp & 3) * 32 + wg * 16) << 16;
   {  // S = small logits
     uint32_t z[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) z[i] = __float_as_uint(-0.01f * float((lane + i) & 63));
-    tmem_st32(tmem + lane_addr + wg * 64, z);
-    tmem_st32(tmem + lane_addr + wg * 64 + 32, z);
+    tmem_st16x2_x32<32>(tmem + lane_addr, z);
+    tmem_st16x2_x32<32>(tmem + lane_addr + 64, z);
     tmem_wait_st();
   }
   uint64_t lsum[2] = {0, 0};
   float m = 0.5f;
+  int vb_next = 0, valid_acc = 0;
+  const uint32_t bar0 = pin_u32(smem_u32(&bars[0])), bar1 = pin_u32(smem_u32(&bars[1]));
   __syncwarp();
   const long long t0 = clock64();
-  for (int it = 0; it < iters; ++it) {
+  for (int it = 0; it < iters + ((FEAT & 8) && wg ? 0 : 0); ++it) {
+    int vb = 0;
+    if constexpr (FEAT & 4) {
+      vb = vb_next;
+      vb_next = __ldg(lut + ((it + 1) & 1023));
+    }
+    if constexpr (FEAT & 2) mbar_wait_a(bar0, 0);
+    tc_fence_after();
     uint32_t sv[64];
-    tmem_ld32(tmem + lane_addr + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
-    tmem_ld32(tmem + lane_addr + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+    if constexpr (FEAT & 16) {
+      tmem_ld32(tmem + (lane_addr & 0xffe00000u) + wg * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+      tmem_ld32(tmem + (lane_addr & 0xffe00000u) + wg * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+    } else {
+      tmem_ld16x2_x64<64>(tmem + lane_addr, sv);
+    }
     tmem_wait_ld();
+    if constexpr (FEAT & 4) {
+      const int valid = min(128, 118800 - vb * 128) - (lane >> 4) * 64;
+      if (valid < 64) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i >= valid) sv[i] = __float_as_uint(-INFINITY);
+      }
+    }
     const uint64_t sc2 = f2_pack(scale, scale), nm2 = f2_pack(-m, -m);
     uint32_t pk[32];
+    float xm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       float x0, x1;
       f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
+      if constexpr (FEAT & 1) xm[i & 3] = fmaxf(xm[i & 3], fmaxf(x0, x1));
+      if constexpr (FEAT & 32)
+        if (poly_at<POLY, PACK>(i)) xm[i & 3] = fmaxf(xm[i & 3], fmaxf(x0, x1));
       float p0, p1;
       if (poly_at<POLY, PACK>(i)) {
         f2_unpack(ex2_poly2(x0, x1), p0, p1);
@@ -63,15 +99,36 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, long long*
       lsum[i & 1] = f2_add(lsum[i & 1], f2_pack(p0, p1));
       pk[i] = PACK ? pack_trunc(p0, p1) : pack_bf16(p0, p1);
     }
-    tmem_st16(tmem + lane_addr + 256 + wg * 32, *reinterpret_cast<const uint32_t(*)[16]>(pk));
-    tmem_st16(tmem + lane_addr + 256 + wg * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
+    if constexpr (FEAT & 1) {
+      float xmax = fmaxf(fmaxf(xm[0], xm[1]), fmaxf(xm[2], xm[3]));
+      xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, 16));
+      if (__any_sync(0xffffffffu, xmax > 1e30f)) m += 1.f;  // never taken
+    }
+    if constexpr (FEAT & 32) {
+      float xmax = fmaxf(fmaxf(xm[0], xm[1]), fmaxf(xm[2], xm[3]));
+      float a0, a1;
+      f2_unpack(f2_add(lsum[0], lsum[1]), a0, a1);
+      if (__any_sync(0xffffffffu, xmax > 20.f || !(a0 + a1 <= 1048576.f))) m += 1.f;  // never taken
+    }
+    if constexpr (FEAT & 16) {
+      tmem_st16(tmem + (lane_addr & 0xffe00000u) + 256 + wg * 32, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+      tmem_st16(tmem + (lane_addr & 0xffe00000u) + 256 + wg * 32 + 16, *reinterpret_cast<const uint32_t(*)[16]>(pk + 16));
+    } else {
+      tmem_st16x2_x32<32>(tmem + lane_addr + 256, pk);
+    }
     tmem_wait_st();
+    if constexpr (FEAT & 2) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_a(bar1);
+    }
     m = m * 1.0000001f;  // loop-carried, like the running max
+    if constexpr (FEAT & 4) valid_acc += vb;
   }
   const long long t1 = clock64();
   float a, b;
   f2_unpack(f2_add(lsum[0], lsum[1]), a, b);
-  out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(a + b + m);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(a + b + m) + valid_acc;
   if (threadIdx.x == 0 && blockIdx.x == 0) *clk = t1 - t0;
   tc_fence_before();
   __syncthreads();
@@ -82,20 +139,30 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, long long*
 int main() {
   uint32_t* out;
   long long* clk;
+  int* lut;
   cudaMalloc(&out, 148 * 256 * 4);
   cudaMallocManaged(&clk, 8);
+  cudaMalloc(&lut, 1024 * 4);
+  cudaMemset(lut, 0, 1024 * 4);
   const int iters = 2000;
-  using KF = void (*)(uint32_t*, int, long long*, float);
+  using KF = void (*)(uint32_t*, int, long long*, float, const int*);
   struct V { const char* name; KF f; } vs[] = {
-      {"all MUFU, cvt.rn", k<0, 0>}, {"poly 1,4,7/8, cvt.rn", k<38, 0>}, {"poly every 3rd, cvt.rn", k<3, 0>},
-      {"poly every 2nd, cvt.rn", k<2, 0>}, {"all MUFU, PRMT trunc", k<0, 1>}, {"poly 1,4,7/8, PRMT trunc", k<38, 1>},
-      {"poly every 3rd, PRMT", k<3, 1>}, {"poly every 2nd, PRMT", k<2, 1>}};
-  for (auto& v : vs)
-    for (int threads : {256}) {
-      for (int rep = 0; rep < 2; ++rep) v.f<<<148, threads>>>(out, iters, clk, 0.1f);
-      cudaDeviceSynchronize();
-      printf("%-26s warps/SMSP=%d: %.0f cycles per block (64 logits/thread)  %s\n", v.name, threads / 128,
-             double(*clk) / iters, cudaGetErrorString(cudaGetLastError()));
-    }
+      {"32x32b ld+exp+st", k<38, 0, 16>},
+      {"ld+exp+st (poly 1,4,7/8)", k<38, 0, 0>},
+      {"+ cheap threshold test", k<38, 0, 32>},
+      {"cheap test + mbar + LUT", k<38, 0, 32 | 6>},
+      {"32x32b + cheap + mbar + LUT", k<38, 0, 32 | 16 | 6>},
+      {"+ threshold test", k<38, 0, 1>},
+      {"+ mbarrier protocol", k<38, 0, 2>},
+      {"+ LUT load / bound", k<38, 0, 4>},
+      {"all of K5's loop", k<38, 0, 7>},
+      {"all, every 3rd poly", k<3, 0, 7>},
+      {"all, all MUFU", k<0, 0, 7>}};
+  for (auto& v : vs) {
+    for (int rep = 0; rep < 2; ++rep) v.f<<<148, 256>>>(out, iters, clk, 0.1f, lut);
+    cudaDeviceSynchronize();
+    printf("%-28s 2 warps/SMSP (16 rows each): %.0f cycles per block  %s\n", v.name, double(*clk) / iters,
+           cudaGetErrorString(cudaGetLastError()));
+  }
   return 0;
 }
