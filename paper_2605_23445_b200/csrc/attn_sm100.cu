@@ -102,12 +102,15 @@ struct Cfg {
   static constexpr int kSmem = kBarOff + 512 + 1024;     // barriers + alignment slack
   static constexpr uint32_t kIdescQK = idesc_bf16_f32(kBM, kBN, false, false);
   static constexpr uint32_t kIdescPV = idesc_bf16_f32(kBM, D, false, true);
-  static constexpr bool kQT = D == 128 && DFS_ATTN_QT;  // Q in TMEM (see DFS_ATTN_QT)
-  // TMEM: S0/P0 [0,128) S1/P1 [128,256) S2/P2 [256,384) O [384,384+D); kQT: two S buffers,
-  // O [256,384), Q [384,448) and [448,512)
-  static constexpr int kSBufs = kQT ? 2 : 3;
-  static constexpr uint32_t kOCol = kQT ? 256 : 384;
-  static constexpr uint32_t kQCol = 384;
+  // Q in TMEM (see DFS_ATTN_QT); at d = 64 its columns are the column-split path's second O
+  static constexpr bool kQT = DFS_ATTN_QT && (D == 128 || DFS_ATTN_ROWSPLIT || !DFS_ATTN_SPLIT_O_D64);
+  // TMEM: S0/P0 [0,128) S1/P1 [128,256) S2/P2 [256,384) O [384,384+D).
+  // kQT, d = 128: two S buffers, O [256,384), Q [384,448) and [448,512);
+  // kQT, d = 64: three S buffers, O [384,448), Q [448,480) and [480,512).
+  static constexpr int kSBufs = kQT && D == 128 ? 2 : 3;
+  static constexpr uint32_t kOCol = kQT && D == 128 ? 256 : 384;
+  static constexpr uint32_t kQCol = D == 128 ? 384 : 448;
+  static constexpr uint32_t kQStride = D / 2;  // TMEM columns of one Q buffer (bf16 pairs)
   static constexpr int kOColsPerWG = D / kWG;
 };
 
@@ -188,8 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const Params p) {
   using C = Cfg<D>;
-  constexpr bool kSplitO = D == 64 && kWG == 2 && DFS_ATTN_SPLIT_O_D64;
-  constexpr bool kRowSplit = D == 128 && kWG == 2 && DFS_ATTN_ROWSPLIT;
+  constexpr bool kRowSplit = kWG == 2 && DFS_ATTN_ROWSPLIT;
+  constexpr bool kSplitO = D == 64 && kWG == 2 && DFS_ATTN_SPLIT_O_D64 && !kRowSplit;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment (SWIZZLE_128B atoms) by offset, so the pointer keeps its shared state space
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (cnt > 0) load_tile(&tm_k, h, int64_t(blk(0)) * kBN);
       if (cnt > 1) load_tile(&tm_k, h, int64_t(blk(1)) * kBN);
       for (int32_t j = 0; j < cnt; ++j) {
-        if constexpr (C::kQT) {
+        if constexpr (C::kSBufs == 2) {
           load_tile(&tm_v, h, int64_t(blk(j)) * kBN);
           if (j + 2 < cnt) load_tile(&tm_k, h, int64_t(blk(j + 2)) * kBN);
         } else {
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Q -> TMEM buffer (tile parity): one 128x256b copy per K step, the same SW128
         // K-major descriptors the SS MMA used. tcgen05.cp and tcgen05.mma execute in issue
         // order, and the buffer's previous user (two tiles back) issued all its QKs before.
-        q_tm = tmem + C::kQCol + (q_phase ? 0u : 64u);
+        q_tm = tmem + C::kQCol + (q_phase ? 0u : C::kQStride);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -442,20 +445,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         release_q();
-        if (cnt > 0) issue_qk();
-        if (cnt > 1) issue_qk();
+      }
+      if (cnt > 0) issue_qk();
+      if (cnt > 1) issue_qk();
+      if constexpr (C::kSBufs == 2) {
         for (int32_t j = 0; j < cnt; ++j) {
           issue_pv(j == 0);
           if (j + 2 < cnt) issue_qk();
         }
       } else {
-        if (cnt > 0) issue_qk();
-        if (cnt > 1) issue_qk();
-        if (cnt <= 2) release_q();
+        if (!C::kQT && cnt <= 2) release_q();
         for (int32_t j = 0; j < cnt; ++j) {
           if (j + 2 < cnt) {
             issue_qk();
-            if (j + 3 == cnt) release_q();
+            if (!C::kQT && j + 3 == cnt) release_q();
           }
           issue_pv(j == 0);
         }
@@ -601,7 +604,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const float inv_l = cnt > 0 ? 1.f / l : 0.f;
       uint32_t ov[D / 2];
-      tmem_ld16x2_x64<D / 2>(tmem + lane_addr + C::kOCol, ov);
+      if constexpr (D == 128)
+        tmem_ld16x2_x64<64>(tmem + lane_addr + C::kOCol, ov);
+      else
+        tmem_ld16x2_x32<32>(tmem + lane_addr + C::kOCol, ov);
       tmem_wait_ld();
       tc_fence_before();
       if (i_row < p.nq) {
@@ -967,13 +973,13 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
   return DFS_OK;
 }
 
-// exp2 split between MUFU and the FMA-pipe polynomial (use_poly): measured per head
-// dimension with tools/k5_cycles.sh and the degree-2 polynomial — d = 128: pairs 1, 4, 7
-// of every 8 (-1.9 % SM cycles vs every 3rd; the positions matter as much as the
-// ratio: pairs 0, 3, 6 gain only 0.5 %), d = 64: every 3rd pair. DFS_ATTN_POLY
-// overrides the default for A/B measurements.
+// exp2 split between MUFU and the FMA-pipe polynomial (use_poly): pairs 1, 4, 7 of every 8,
+// measured with tools/k5_cycles.sh and the degree-2 polynomial (column-split kernel, d = 128:
+// -1.9 % SM cycles vs every 3rd pair; the positions matter as much as the ratio: pairs 0, 3, 6
+// gain only 0.5 %; row-split kernel, d = 64: -0.6 % vs every 3rd, every 2nd +8 %).
+// DFS_ATTN_POLY overrides the default for A/B measurements.
 template <int D>
-constexpr int kDefaultPoly = D == 128 ? 38 : 3;
+constexpr int kDefaultPoly = 38;
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
