@@ -136,6 +136,66 @@ __global__ void __launch_bounds__(256, 1) k(uint32_t* out, int iters, long long*
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+
+// NL logits per thread (64 or 32) with 128 * WPS threads: WPS warps per SMSP. NL = 32: warp pairs
+// of a row group take column halves (16x32bx2.x32 at columns 32 * half + {0, 64}).
+template <int NL, int WPS>
+__global__ void __launch_bounds__(128 * WPS, 1) kw(uint32_t* out, int iters, long long* clk, float scale) {
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int grp = warp >> 2;                   // 0 .. WPS-1
+  const int hf = NL == 64 ? grp : (grp >> 1);  // row half
+  const int cs = NL == 64 ? 0 : (grp & 1);     // column half (NL = 32)
+  const uint32_t tmem = tbase, lane_addr = uint32_t((warp & 3) * 32 + hf * 16) << 16;
+  uint64_t lsum[2] = {0, 0};
+  float m = 0.5f;
+  __syncwarp();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    uint32_t sv[NL];
+    if constexpr (NL == 64)
+      tmem_ld16x2_x64<64>(tmem + lane_addr, sv);
+    else
+      tmem_ld16x2_x32<64>(tmem + lane_addr + cs * 32, sv);
+    tmem_wait_ld();
+    const uint64_t sc2 = f2_pack(scale, scale), nm2 = f2_pack(-m, -m);
+    uint32_t pk[NL / 2];
+#pragma unroll
+    for (int i = 0; i < NL / 2; ++i) {
+      float x0, x1;
+      f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
+      float p0, p1;
+      if (poly_at<38, 0>(i)) {
+        f2_unpack(ex2_poly2(x0, x1), p0, p1);
+      } else {
+        p0 = ex2(x0);
+        p1 = ex2(x1);
+      }
+      lsum[i & 1] = f2_add(lsum[i & 1], f2_pack(p0, p1));
+      pk[i] = pack_bf16(p0, p1);
+    }
+    if constexpr (NL == 64)
+      tmem_st16x2_x32<32>(tmem + lane_addr + 256, pk);
+    else
+      tmem_st16x2_x16<32>(tmem + lane_addr + 256 + cs * 16, pk);
+    tmem_wait_st();
+    m = m * 1.0000001f;
+  }
+  const long long t1 = clock64();
+  float a, b;
+  f2_unpack(f2_add(lsum[0], lsum[1]), a, b);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(a + b + m);
+  if (threadIdx.x == 0 && blockIdx.x == 0) *clk = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
 int main() {
   uint32_t* out;
   long long* clk;
@@ -158,6 +218,17 @@ int main() {
       {"all of K5's loop", k<38, 0, 7>},
       {"all, every 3rd poly", k<3, 0, 7>},
       {"all, all MUFU", k<0, 0, 7>}};
+  {
+    using KW = void (*)(uint32_t*, int, long long*, float);
+    struct W { const char* name; KW f; int threads; } ws[] = {
+        {"2 warps/SMSP x 64 logits", kw<64, 2>, 256}, {"4 warps/SMSP x 32 logits", kw<32, 4>, 512}};
+    for (auto& w : ws) {
+      for (int rep = 0; rep < 2; ++rep) w.f<<<148, w.threads>>>(out, iters, clk, 0.1f);
+      cudaDeviceSynchronize();
+      printf("%-28s: %.0f cycles per block (4096 exps per SMSP)  %s\n", w.name, double(*clk) / iters,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  }
   for (auto& v : vs) {
     for (int rep = 0; rep < 2; ++rep) v.f<<<148, 256>>>(out, iters, clk, 0.1f, lut);
     cudaDeviceSynchronize();

@@ -95,6 +95,23 @@ __global__ void k(float* out, int iters, long long* clk) {
         a[i] = fmax2(a[i], s1);
       }
       if (MODE == 11) u[i] = shladd(u[i], u[(i + 1) & 7]);
+      if (MODE == 12) {  // 1 MUFU + 1 F2FP (shared XU pipe?)
+        a[i] = ex2(a[i]);
+        u[i] = cvt_bf16x2(__uint_as_float(u[i]), s1);
+      }
+      if (MODE == 13) {  // 1 MUFU + 2 F2FP
+        a[i] = ex2(a[i]);
+        u[i] = cvt_bf16x2(__uint_as_float(u[i]), s1);
+        u[i] = cvt_bf16x2(__uint_as_float(u[i]), s2);
+      }
+      if (MODE == 14) {  // 1 F2FP + 1 FFMA2
+        u[i] = cvt_bf16x2(__uint_as_float(u[i]), s1);
+        p[i] = f2fma(p[i], c1, c2);
+      }
+      if (MODE == 15) {  // 1 F2FP + 1 FMNMX3
+        u[i] = cvt_bf16x2(__uint_as_float(u[i]), s1);
+        a[i] = fmax3(a[i], s1, s2);
+      }
     }
   }
   long long t1 = clock64();
@@ -112,11 +129,11 @@ int main() {
   cudaMallocManaged(&clk, 8);
   const int iters = 2048;
   const char* names[] = {"FFMA", "FFMA2", "FADD2", "FMNMX", "FMNMX3", "F2FP.BF16", "IMAD", "MUFU.EX2",
-                         "EX2+FFMA2", "EX2+3xFFMA2", "FFMA2+FMNMX", "SHL+IADD"};
+                         "EX2+FFMA2", "EX2+3xFFMA2", "FFMA2+FMNMX", "SHL+IADD", "EX2+F2FP", "EX2+2xF2FP", "F2FP+FFMA2", "F2FP+FMNMX3"};
   using KF = void (*)(float*, int, long long*);
-  KF ks[] = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>, k<8>, k<9>, k<10>, k<11>};
-  for (int mode = 0; mode < 12; ++mode)
-    for (int threads : {128, 256, 512}) {
+  KF ks[] = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>, k<6>, k<7>, k<8>, k<9>, k<10>, k<11>, k<12>, k<13>, k<14>, k<15>};
+  for (int mode = 0; mode < 16; ++mode)
+    for (int threads : {256}) {
       for (int rep = 0; rep < 2; ++rep) ks[mode]<<<148, threads>>>(out, iters, clk);
       cudaDeviceSynchronize();
       const double warps_per_smsp = threads / 128.0;
