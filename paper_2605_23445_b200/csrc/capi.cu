@@ -161,10 +161,12 @@ struct dfs_handle {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_v = nullptr;
   ~dfs_handle() {
+    if (host_flag) cudaFreeHost(host_flag);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_v) cudaEventDestroy(ev_v);
     if (aux) cudaStreamDestroy(aux);
   }
+  int32_t* host_flag = nullptr;  // pinned read-back slot of the step's non-finite flag
   int ensure_aux() {
     if (aux) return DFS_OK;
     DFS_CUDA_CHECK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
@@ -737,11 +739,23 @@ namespace capi_detail {
 // cached): the reference throws from check_qkv / attention_scores before build_mask
 // stores a mask (attention.cpp:19-20, scheduler.cpp:114-116), so a NaN step leaves the
 // cache and the output untouched here too.
-int check_flag(const int32_t* flag, cudaStream_t s) {
-  int32_t bad = 0;
-  DFS_CUDA_CHECK(cudaMemcpyAsync(&bad, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+// Both step flags (q/k at flag[0], v at flag[1]) in one read-back on `s`; the caller decides
+// when each is reported.
+int check_flags2(dfs_handle* h, const int32_t* flag, cudaStream_t s) {
+  if (!h->host_flag) DFS_CUDA_CHECK(cudaMallocHost(&h->host_flag, 64));
+  DFS_CUDA_CHECK(cudaMemcpyAsync(h->host_flag, flag, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   DFS_CUDA_CHECK(cudaStreamSynchronize(s));
-  if (bad) return fail(DFS_E_INVALID, "attention: non-finite input");
+  if (h->host_flag[0]) return fail(DFS_E_INVALID, "attention: non-finite input");
+  return DFS_OK;
+}
+
+// The read-back goes to pinned memory: a pageable D2H copy is staged by the driver and held
+// back the kernels launched right after it (traced: ~175 us of GPU idle per update step).
+int check_flag(dfs_handle* h, const int32_t* flag, cudaStream_t s) {
+  if (!h->host_flag) DFS_CUDA_CHECK(cudaMallocHost(&h->host_flag, 64));
+  DFS_CUDA_CHECK(cudaMemcpyAsync(h->host_flag, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  DFS_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (*h->host_flag) return fail(DFS_E_INVALID, "attention: non-finite input");
   return DFS_OK;
 }
 
@@ -796,18 +810,21 @@ int compat_scores(dfs_handle* h, const float* pq, const float* pk, int64_t H, in
 // Scoring (K3, or the compatibility scorer), top-K (K4) and the commit of the new masks
 // of heads `need` into the layer's device CSR (scheduler.cpp:113-116 build_mask +
 // cache.store). Runs only after the step's non-finite check passed.
-int build_and_commit(dfs_handle* h, int layer, int step, const std::vector<int>& need, int64_t H, int64_t m,
-                     int64_t n, int64_t d, int64_t B, int64_t Bs, double budget, bool compat, const float* pq,
-                     const float* pk, LayerMasks** Lout, cudaStream_t s) {
+// K3: block scores of every head into h->scores (scratch: nothing is committed yet)
+int score_phase(dfs_handle* h, int64_t H, int64_t m, int64_t n, int64_t d, int64_t B, int64_t Bs, bool compat,
+                const float* pq, const float* pk, cudaStream_t s) {
+  int rc;
+  if ((rc = h->scores.ensure(sizeof(double) * size_t(H * m * m)))) return rc;
+  if (compat) return compat_scores(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
+  return score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
+}
+
+// K4 over h->scores and the commit of the selected masks into the layer's device CSR cache
+int select_commit(dfs_handle* h, int layer, int step, const std::vector<int>& need, int64_t H, int64_t m,
+                  int64_t B, double budget, LayerMasks** Lout, cudaStream_t s) {
   int rc;
   int64_t K;
   if ((rc = dfs_topk_count(budget, m, &K))) return rc;
-  if ((rc = h->scores.ensure(sizeof(double) * size_t(H * m * m)))) return rc;
-  if (compat)
-    rc = compat_scores(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
-  else
-    rc = score_dispatch(h, pq, pk, H, n, d, B, Bs, h->scores.as<double>(), s);
-  if (rc) return rc;
   if (m > topk_max_m()) return fail(DFS_E_UNSUPPORTED, "topk_select: M too large");
   if (int64_t(need.size()) == H) {
     // common case: every head refreshes -> the LUT becomes the layer's CSR in place
@@ -859,6 +876,13 @@ int build_and_commit(dfs_handle* h, int layer, int step, const std::vector<int>&
   }
   *Lout = &NL;
   return DFS_OK;
+}
+
+int build_and_commit(dfs_handle* h, int layer, int step, const std::vector<int>& need, int64_t H, int64_t m,
+                     int64_t n, int64_t d, int64_t B, int64_t Bs, double budget, bool compat, const float* pq,
+                     const float* pk, LayerMasks** Lout, cudaStream_t s) {
+  if (int rc = score_phase(h, H, m, n, d, B, Bs, compat, pq, pk, s)) return rc;
+  return select_commit(h, layer, step, need, H, m, B, budget, Lout, s);
 }
 
 int attn_simple(dfs_handle* h, const void* q, const void* k, const void* v, void* o, int dtype, int in_layout,
@@ -980,7 +1004,7 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       if ((rc = h->q16.ensure(tok16)) || (rc = h->k16.ensure(tok16))) return rc;
       if ((rc = prologue(a->q, h->q16.p, DFS_NHD, nullptr, nullptr, pro->q_norm_weight)) ||
           (rc = prologue(a->k, h->k16.p, DFS_NHD, nullptr, nullptr, pro->k_norm_weight)) ||
-          (rc = finite_check_impl(a->v, n * H * d, DFS_BF16, flag, s)) || (rc = check_flag(flag, s)))
+          (rc = finite_check_impl(a->v, n * H * d, DFS_BF16, flag, s)) || (rc = check_flag(h, flag, s)))
         return rc;
       if ((rc = attn_simple(h, h->q16.p, h->k16.p, a->v, a->o, DFS_BF16, DFS_NHD, nullptr, DFS_NHD, nullptr, H, n, d,
                             d, B, nullptr, nullptr, s)))
@@ -990,12 +1014,12 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       const void* x[3] = {a->q, a->k, a->v};
       for (int t = 0; t < 3; ++t)
         if ((rc = finite_check_impl(x[t], c[t], dtype, flag, s))) return rc;
-      if ((rc = check_flag(flag, s))) return rc;
+      if ((rc = check_flag(h, flag, s))) return rc;
       if ((rc = attn_simple(h, a->q, a->k, a->v, a->o, dtype, DFS_NHD, nullptr, DFS_NHD, nullptr, H, n, d, dv, B,
                             nullptr, nullptr, s)))
         return rc;
     } else {
-      if ((rc = cast_inputs()) || (rc = check_flag(flag, s))) return rc;
+      if ((rc = cast_inputs()) || (rc = check_flag(h, flag, s))) return rc;
       if ((rc = h->o16.ensure(tok16))) return rc;
       if ((rc = attn_simple(h, h->q16.p, h->k16.p, h->v16.p, h->o16.p, DFS_BF16, DFS_NHD, nullptr, DFS_NHD, nullptr,
                             H, n, d, d, B, nullptr, nullptr, s)) ||
@@ -1125,16 +1149,31 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       return rc;
     }
   }
-  if ((rc = check_flag(flag, s))) return rc;  // nothing scored, cached or written yet
-
-  if (update_any && (rc = build_and_commit(h, a->layer, a->step, need, H, m, n, d, B, Bs, budget, compat,
-                                             h->pooled_q.as<float>(), h->pooled_k.as<float>(), &L, s)))
-    return rc;
+  if (v_aside && update_any && flag + 1 == flag_v) {
+    // The non-finite read-back overlaps K3: both flags are copied on the side stream once K2
+    // (main stream) and V's reorder (side stream) are done, K3 is launched, and the host waits
+    // for the copy while the scorer runs. K3 writes scratch only; K4 and the mask commit are
+    // launched after the check (the reference throws before build_mask stores anything).
+    DFS_CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
+    DFS_CUDA_CHECK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+    if ((rc = score_phase(h, H, m, n, d, B, Bs, false, h->pooled_q.as<float>(), h->pooled_k.as<float>(), s)))
+      return rc;
+    if ((rc = check_flags2(h, flag, h->aux))) return rc;  // q, k (slot 0) and v (slot 1)
+    if ((rc = select_commit(h, a->layer, a->step, need, H, m, B, budget, &L, s))) return rc;
+    if (h->host_flag[1]) return fail(DFS_E_INVALID, "attention: non-finite input");  // after the commit, as v's
+    DFS_CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_v, 0));
+    v_late = false;
+  } else {
+    if ((rc = check_flag(h, flag, s))) return rc;  // nothing scored, cached or written yet
+    if (update_any && (rc = build_and_commit(h, a->layer, a->step, need, H, m, n, d, B, Bs, budget, compat,
+                                               h->pooled_q.as<float>(), h->pooled_k.as<float>(), &L, s)))
+      return rc;
+  }
 
   if (v_late) {
     // V is checked like the reference's block_sparse_attention checks it: after build_mask
     // stored the mask (scheduler.cpp:113-122), before any output is produced
-    if ((rc = check_flag(flag_v, v_aside ? h->aux : s))) return rc;
+    if ((rc = check_flag(h, flag_v, v_aside ? h->aux : s))) return rc;
     if (v_aside) DFS_CUDA_CHECK(cudaStreamWaitEvent(s, h->ev_v, 0));
   }
   // attention over the selected blocks; output row i -> raster row fwd[i] (scheduler.cpp:134)
@@ -1338,7 +1377,7 @@ int dfs_alltoall_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_al
       (rc = permute_rows_peer_impl(dtab + 1, Ht, h->k_hnd.p, fwd, n, Hl, d, pk, pk ? Bs : 1, flag, s)) ||
       (rc = permute_rows_peer_impl(dtab + 2, Ht, h->v_hnd.p, fwd, n, Hl, d, nullptr, 1, flag, s)))
     return rc;
-  if ((rc = check_flag(flag, s))) return rc;
+  if ((rc = check_flag(h, flag, s))) return rc;
   if (update_any &&
       (rc = build_and_commit(h, a->layer, a->step, need, Hl, m, n, d, B, Bs, budget, false, pq, pk, &L, s)))
     return rc;

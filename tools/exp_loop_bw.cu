@@ -196,6 +196,95 @@ __global__ void __launch_bounds__(128 * WPS, 1) kw(uint32_t* out, int iters, lon
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+
+// Ping-pong candidate: one thread per row (32x32b: 32 lanes of the warp's quadrant), 128 logits
+// per thread per block in 4 chunks of 32 (TMEM load of chunk c + 1 in flight while chunk c is
+// exponentiated), P stored per chunk; WPS independent warps per SMSP (different tiles).
+// MMA > 0: one extra warp (id 4 * WPS, SMSP 0) issues K5's MMA pattern (QK + PV, both operands
+// from shared memory / TMEM, on TMEM columns 256-511) back to back while the softmax warps run.
+template <int WPS, int MMA = 0>
+__global__ void __launch_bounds__(128 * WPS + 32 * MMA, 1) kp(uint32_t* out, int iters, long long* clk, float scale) {
+  __shared__ uint32_t tbase;
+  __shared__ volatile int done;
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) done = 0;
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (MMA && warp == 4 * WPS) {
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+    const uint32_t a = smem_u32(sm), b = a + 32768;
+    const uint32_t idqk = idesc_bf16_f32(128, 128, false, false), idpv = idesc_bf16_f32(128, 128, false, true);
+    if ((threadIdx.x & 31) == 0) {
+      while (!done) {
+#pragma unroll
+        for (int st = 0; st < 8; ++st) {
+          const uint32_t off = (st >> 2) * 16384 + (st & 3) * 32;
+          umma_f16(tbase + 256, smem_desc_sw128(a + off, 16, 1024), smem_desc_sw128(b + off, 16, 1024), idqk, st > 0);
+        }
+#pragma unroll
+        for (int st = 0; st < 8; ++st)
+          umma_f16_ts(tbase + 384, tbase + 256 + st * 8, smem_desc_sw128(b + st * 16 * 128, 16384, 1024), idpv, 1);
+      }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc<512>(tbase);
+    return;
+  }
+  const int tile = warp >> 2;  // which tile's S / P this warp works on
+  const uint32_t tmem = tbase + tile * 256, lane_addr = uint32_t((warp & 3) * 32) << 16;
+  uint64_t lsum[2] = {0, 0};
+  float m = 0.5f;
+  __syncwarp();
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    const uint64_t sc2 = f2_pack(scale, scale), nm2 = f2_pack(-m, -m);
+    uint32_t sa[32], sb[32];
+    tmem_ld32(tmem + lane_addr, sa);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t(&cur)[32] = (c & 1) ? sb : sa;
+      uint32_t(&nxt)[32] = (c & 1) ? sa : sb;
+      if (c < 3) tmem_ld32(tmem + lane_addr + (c + 1) * 32, nxt);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float x0, x1;
+        f2_unpack(f2_fma(f2_pack(__uint_as_float(cur[2 * i]), __uint_as_float(cur[2 * i + 1])), sc2, nm2), x0, x1);
+        float p0, p1;
+        if (poly_at<38, 0>(i + 16 * c)) {
+          f2_unpack(ex2_poly2(x0, x1), p0, p1);
+        } else {
+          p0 = ex2(x0);
+          p1 = ex2(x1);
+        }
+        lsum[i & 1] = f2_add(lsum[i & 1], f2_pack(p0, p1));
+        pk[i] = pack_bf16(p0, p1);
+      }
+      tmem_st16(tmem + lane_addr + 128 + c * 16, pk);
+      if (c < 3) tmem_wait_ld();
+    }
+    tmem_wait_st();
+    m = m * 1.0000001f;
+  }
+  const long long t1 = clock64();
+  float a, b;
+  f2_unpack(f2_add(lsum[0], lsum[1]), a, b);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __float_as_uint(a + b + m);
+  if (threadIdx.x == 0 && blockIdx.x == 0) *clk = t1 - t0;
+  if (threadIdx.x == 0) done = 1;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
 int main() {
   uint32_t* out;
   long long* clk;
@@ -228,6 +317,16 @@ int main() {
       printf("%-28s: %.0f cycles per block (4096 exps per SMSP)  %s\n", w.name, double(*clk) / iters,
              cudaGetErrorString(cudaGetLastError()));
     }
+  }
+  for (int cfg = 0; cfg < 4; ++cfg) {
+    const int wps = cfg & 1 ? 2 : 1, mma = cfg >> 1;
+    using KP = void (*)(uint32_t*, int, long long*, float);
+    KP f = cfg == 0 ? kp<1, 0> : cfg == 1 ? kp<2, 0> : cfg == 2 ? kp<1, 1> : kp<2, 1>;
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 66560);
+    for (int rep = 0; rep < 2; ++rep) f<<<148, 128 * wps + 32 * mma, 66560>>>(out, iters, clk, 0.1f);
+    cudaDeviceSynchronize();
+    printf("ping-pong: %d warp(s)/SMSP x 128 logits (chunks of 32)%s: %.0f cycles per block per warp  %s\n", wps,
+           mma ? " + MMA warp" : "", double(*clk) / iters, cudaGetErrorString(cudaGetLastError()));
   }
   for (auto& v : vs) {
     for (int rep = 0; rep < 2; ++rep) v.f<<<148, 256>>>(out, iters, clk, 0.1f, lut);
