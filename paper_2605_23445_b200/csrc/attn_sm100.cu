@@ -181,6 +181,8 @@ __device__ __forceinline__ constexpr bool use_poly(int i) {
     return false;
   } else if constexpr (POLY == 38) {
     return (0x92u >> (i % 8)) & 1u;  // pairs 1, 4, 7 of each 8
+  } else if constexpr (POLY == 516) {
+    return (0x2492u >> (i % 16)) & 1u;  // pairs 1, 4, 7, 10, 13 of each 16
   } else {
     return i % POLY == POLY - 1;
   }
@@ -973,13 +975,14 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
   return DFS_OK;
 }
 
-// exp2 split between MUFU and the FMA-pipe polynomial (use_poly): pairs 1, 4, 7 of every 8,
-// measured with tools/k5_cycles.sh and the degree-2 polynomial (column-split kernel, d = 128:
-// -1.9 % SM cycles vs every 3rd pair; the positions matter as much as the ratio: pairs 0, 3, 6
-// gain only 0.5 %; row-split kernel, d = 64: -0.6 % vs every 3rd, every 2nd +8 %).
-// DFS_ATTN_POLY overrides the default for A/B measurements.
+// exp2 split between MUFU and the FMA-pipe polynomial (use_poly), measured with
+// tools/k5_cycles.sh (SM cycles, degree-2 polynomial, row-split kernel): d = 128 runs pairs
+// 1, 4, 7, 10, 13 of every 16 (31 %): HY -4.1 % vs 1, 4, 7 of every 8, -1.2 % vs every 3rd;
+// 0, 3, 6, 9, 12 / 2, 5, 8, 11, 14 of 16 and 4 or 6 of 16 are 2-4 % slower — the placement
+// in the compiler's schedule matters as much as the ratio. d = 64 keeps 1, 4, 7 of every 8
+// (5 of 16 is +3 % there). DFS_ATTN_POLY overrides the default for A/B measurements.
 template <int D>
-constexpr int kDefaultPoly = 38;
+constexpr int kDefaultPoly = D == 128 ? 516 : 38;
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
@@ -1024,6 +1027,7 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
       case 2: rc = launch_kernel<D, 2>(mq, mk, mv, p, stream); break;
       case 3: rc = launch_kernel<D, 3>(mq, mk, mv, p, stream); break;
       case 38: rc = launch_kernel<D, 38>(mq, mk, mv, p, stream); break;
+      case 516: rc = launch_kernel<D, 516>(mq, mk, mv, p, stream); break;
       default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
     }
   }
