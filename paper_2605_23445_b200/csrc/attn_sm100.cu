@@ -1088,17 +1088,6 @@ bool attn_sm100_supports(const dfs_attn_args& a) {
 }
 
 int sparse_attn_b64(const dfs_attn_args& a, float scale, cudaStream_t stream);  // attn_b64.cu
-int sparse_attn_pp(const dfs_attn_args& a, float scale, cudaStream_t stream);   // attn_pp.cu
-
-// B = 128: the two-tile ping-pong kernel (attn_pp.cu) or this file's one-tile kernel;
-// DFS_ATTN_PP=0/1 overrides the default for A/B measurements.
-#ifndef DFS_ATTN_PP_DEFAULT
-#define DFS_ATTN_PP_DEFAULT 0
-#endif
-static bool use_pp() {
-  static const bool pp = getenv("DFS_ATTN_PP") ? atoi(getenv("DFS_ATTN_PP")) != 0 : DFS_ATTN_PP_DEFAULT;
-  return pp;
-}
 
 int sparse_attn_sm100(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   if (a.block == 64) {
@@ -1106,7 +1095,6 @@ int sparse_attn_sm100(const dfs_attn_args& a, float scale, cudaStream_t stream) 
     return sparse_attn_b64(a, scale, stream);
   }
   if (a.block != 128) return fail(DFS_E_UNSUPPORTED, "attn_sm100: block must be 64 or 128");
-  if (use_pp()) return sparse_attn_pp(a, scale, stream);
   if (a.d == 128) return launch<128>(a, scale, stream);
   if (a.d == 64) return launch<64>(a, scale, stream);
   return fail(DFS_E_UNSUPPORTED, "attn_sm100: d must be 64 or 128");
