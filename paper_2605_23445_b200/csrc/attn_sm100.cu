@@ -6,25 +6,26 @@
 // (top-K LUT, or every block for dense / cross attention), so masked blocks
 // cost neither bytes nor FLOPs.
 //
-// Warp roles (128 * kWG + 64 threads; kWG = 2 -> 320). The MMA issuer takes the HIGHEST warp
-// id: the SMSP arbiter issues highest-id first, and the issuer shares its SMSP with two
-// softmax warps — at the lowest id it saw P_j ~500 cycles late and was as slow to issue PV_j.
-//   warp 0      TMA producer: Q tile (TMA tile::gather4 of raster rows when the
-//               reorder is fused), then K_0, K_1, K_2, V_0, K_3, V_1, ... into a
-//               ring of kStages smem slots (SWIZZLE_128B boxes of 128 x 64).
-//   warp 9      MMA issuer (one elected lane): S_j = Q K_j^T into one of three
-//               TMEM S buffers (QK runs two blocks ahead of PV, so the tensor pipe
-//               always has work queued behind each PV), then O += P_j V_j with P_j
-//               read straight from TMEM (bf16, aliasing S_j) and O resident in TMEM.
-//   warps 1-8   softmax / correction / epilogue: kWG warpgroups split the 128 key
-//               columns of every query row (TMEM lane); each thread handles
-//               128 / kWG logits per block and the row max is exchanged through
-//               shared memory with one named barrier per block. Online softmax in
-//               the log2 domain, exp2 split between MUFU and an FMA-pipe polynomial;
-//               O is rescaled in TMEM only when the running max grows by > 2^8 (the
-//               final normalisation uses the same stale max for O and l, so this is
-//               exact). The epilogue writes each output row straight to its raster
-//               position out_rows[i] — the unpermute (scheduler.cpp:134) is fused here.
+// Warp roles (320 threads):
+//   warp 0      TMA producer: the Q tile (TMA tile::gather4 of raster rows when the
+//               reorder is fused), then K_0, K_1, ... / V_0, V_1, ... into one ring of
+//               kStages smem slots (SWIZZLE_128B boxes of 128 x 64) in the MMA warp's order.
+//   warp 9      MMA issuer (one elected lane): Q copied once per tile into TMEM
+//               (tcgen05.cp), S_j = Q K_j^T with A from TMEM into one of the TMEM S
+//               buffers, O += P_j V_j with P_j read straight from TMEM (bf16, aliasing S_j).
+//   warps 1-8   softmax / epilogue. Default (row split): the two warps of a TMEM lane
+//               quadrant own 16 query rows each, a thread pair per row (key columns
+//               0-63 / 64-127, tcgen05.ld 16x32bx2), so a row's max is one shuffle and no
+//               warp waits for another. The running max is stale by design: the
+//               exponentials use it directly and a block that raises it by > 2^8 rescales
+//               O in TMEM and recomputes (exact: O and l share the stale max). exp2 is
+//               split between MUFU and a degree-2 FMA-pipe polynomial. The epilogue writes
+//               each output row straight to its raster position out_rows[i] — the
+//               unpermute (scheduler.cpp:134) is fused here.
+//               DFS_ATTN_ROWSPLIT=0 builds the earlier column split (two warpgroups split
+//               the 128 key columns, row max exchanged through shared memory per block).
+// TMEM, row split: d = 128: S0/P0 [0,128) S1/P1 [128,256) O [256,384) Q [384,448) [448,512);
+// d = 64: S0..S2 [0,384) O [384,448) Q [448,480) [480,512).
 // Padded keys of the last partial block get -inf logits; padded query rows
 // are computed on TMA zero-fill and never stored (attention.cpp:146-152).
 #include <cuda.h>
@@ -467,8 +468,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if constexpr (kRowSplit) {
-    // ======================= softmax / epilogue, row split (d = 128) ====================
-    // warp w: TMEM lane quadrant w & 3, row half (w - 2) >> 2: rows 32 (w & 3) + 16 half + [0, 16).
+    // ============================ softmax / epilogue, row split ===========================
+    // warp w (1..8): TMEM lane quadrant w & 3, row half (w - 1) >> 2: rows 32 (w & 3) + 16 half + [0, 16).
     // Lane l: row (l & 15) of those, key columns 64 (l >> 4) + [0, 64) of every block.
     const int hf = (warp - 1) >> 2, ch = lane >> 4;
     const int r = (warp & 3) * 32 + hf * 16 + (lane & 15);  // query row within the tile == TMEM lane

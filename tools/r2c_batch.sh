@@ -2,7 +2,7 @@
 # Round-2 measurement batch on one B200 after the K5 row-split rework (run from the repo root):
 # GPU tests + smoke, bench lines (HY with the CPU baseline, C, W4, W7, W4/W7 trajectories),
 # the reference arm, launch list + ncu --set full of one HY update step, sanitizers.
-OUT=gpurun_out/r2c; mkdir -p $OUT
+OUT=gpurun_out/${R2_OUT:-r2c}; mkdir -p $OUT
 timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/summary.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/summary.txt
 timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench_HY.json 2> $OUT/bench_HY.err
