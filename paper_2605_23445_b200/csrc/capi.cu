@@ -1114,6 +1114,19 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
       att_q = q;
       pq = pk = nullptr;  // already pooled
     }
+    // V's reordered copy is read only by K5: on the bf16 path it runs on the side stream from
+    // the start of the step, next to the q and k passes (the q pass alone does not saturate
+    // HBM) and under the flag read-back and K3/K4
+    if (!pro && dtype == DFS_BF16) {
+      if ((rc = h->ensure_aux())) return rc;
+      DFS_CUDA_CHECK(cudaEventRecord(h->ev_fork, s));  // after the flag reset
+      DFS_CUDA_CHECK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
+      if ((rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag_v, false,
+                                  h->aux)))
+        return rc;
+      DFS_CUDA_CHECK(cudaEventRecord(h->ev_v, h->aux));
+      v_aside = v_late = true;
+    }
     if (pro) {
       // QK-norm / RoPE fused into the reorder: the transformed q gets a reordered copy
       // (K5 then loads Q tiles instead of gathering raster rows), k goes to k_hnd
@@ -1133,21 +1146,9 @@ int dfs_run_step(dfs_handle* h, const dfs_schedule* sched, const dfs_step_args* 
     if (!pro && (rc = permute_rows_impl(k, DFS_NHD, h->k_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, pk, pk ? Bs : 1,
                                         flag, false, s)))
       return rc;
-    if (!pro && dtype == DFS_BF16) {
-      // V's reordered copy is read only by K5: on an update step it runs on the side stream
-      // under the flag read-back and K3/K4 (compute-bound), off the critical path
-      if ((rc = h->ensure_aux())) return rc;
-      DFS_CUDA_CHECK(cudaEventRecord(h->ev_fork, s));
-      DFS_CUDA_CHECK(cudaStreamWaitEvent(h->aux, h->ev_fork, 0));
-      if ((rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1, flag_v, false,
-                                  h->aux)))
-        return rc;
-      DFS_CUDA_CHECK(cudaEventRecord(h->ev_v, h->aux));
-      v_aside = v_late = true;
-    } else if (!pro && (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr, 1,
-                                               flag, false, s))) {
+    if (!pro && !v_aside && (rc = permute_rows_impl(v, DFS_NHD, h->v_hnd.p, DFS_HND, DFS_BF16, fwd, n, H, d, nullptr,
+                                                    1, flag, false, s)))
       return rc;
-    }
   }
   if (v_aside && update_any && flag + 1 == flag_v) {
     // The non-finite read-back overlaps K3: both flags are copied on the side stream once K2
