@@ -45,7 +45,6 @@ constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-ro
 
 template <int D, int BN>
 struct Cfg {
-  static constexpr int kBN = BN;
   static constexpr int kCPT = BN / kWG;                  // key columns (logits) per softmax thread per block
   static constexpr int kChunks = D / 64;                 // 128-byte swizzle chunks per row
   static constexpr int kTileBytes = kBM * D * 2;         // the Q tile
@@ -516,7 +515,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (i < p.nq) {
         __nv_bfloat16* dst = p.out + row_offset(p.out_layout, p.nq, p.heads, D, h, orow) + wg * kOC;
-#pragma unroll
         // 32-byte stores (STG.256): half the store instructions of 16-byte ones; the store
         // issue at the tile boundary is what holds the warps there
         uint32_t w[kOC / 2];

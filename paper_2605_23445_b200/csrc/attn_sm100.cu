@@ -49,7 +49,7 @@ constexpr int kBN = 128;         // keys per block
 #define DFS_ATTN_WG 2
 #endif
 constexpr int kWG = DFS_ATTN_WG;           // softmax warpgroups splitting the 128 key columns
-constexpr int kCPT = 128 / kWG;            // key columns (logits) per softmax thread per block
+[[maybe_unused]] constexpr int kCPT = 128 / kWG;  // column split: key columns (logits) per softmax thread per block
 constexpr int kSoftmaxThreads = 128 * kWG;
 constexpr int kThreads = 64 + kSoftmaxThreads;
 constexpr int kMmaWarp = kSoftmaxThreads / 32 + 1;  // 9; softmax warps 1 .. kSoftmaxThreads / 32
@@ -58,7 +58,7 @@ constexpr uint32_t kTmemCols = 512;
 #define DFS_ATTN_RESCALE_LOG2 8.0f
 #endif
 constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
-constexpr uint32_t kBarRows = 2;           // named barriers 2..5: one per 32-row group (0 = __syncthreads)
+[[maybe_unused]] constexpr uint32_t kBarRows = 2;  // column split: named barriers 2..5: one per 32-row group (0 = __syncthreads)
 // d = 64: the two softmax warpgroups run DECOUPLED (no per-block row-max exchange): each
 // keeps its own running max / sum for its 64 key columns and its own O accumulator in
 // TMEM (O_0 at column 384, O_1 at 448: 3 S buffers + 2 x 64 columns = 512), PV_j is two
@@ -112,7 +112,6 @@ struct Cfg {
   static constexpr uint32_t kOCol = kQT && D == 128 ? 256 : 384;
   static constexpr uint32_t kQCol = D == 128 ? 384 : 448;
   static constexpr uint32_t kQStride = D / 2;  // TMEM columns of one Q buffer (bf16 pairs)
-  static constexpr int kOColsPerWG = D / kWG;
 };
 
 struct Params {
@@ -644,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ============================ softmax / epilogue ============================
     // kWG warpgroups split the 128 key columns of each block (128 / kWG each); a thread
     // owns one query row (TMEM lane) of its 32-column slice.
+    constexpr int kOColsPerWG = D / kWG;  // output columns per warpgroup
     const int wg = (warp - 1) >> 2;                    // key columns [kCPT*wg, kCPT*wg + kCPT)
     const int r = (warp & 3) * 32 + lane;              // query row within the tile == TMEM lane
     const uint32_t lane_addr = uint32_t((warp & 3) * 32) << 16;
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           lsum[0] = f2_mul(lsum[0], a2);
           lsum[1] = f2_mul(lsum[1], a2);
           m = m_new;
-          const uint32_t o_addr = tmem + lane_addr + C::kOCol + wg * (kSplitO ? D : C::kOColsPerWG);
+          const uint32_t o_addr = tmem + lane_addr + C::kOCol + wg * (kSplitO ? D : kOColsPerWG);
           if constexpr (kSplitO) {  // this warpgroup's own O: all d columns
 #pragma unroll
             for (int c = 0; c < D; c += 32) {
@@ -747,9 +747,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
               tmem_st32(o_addr + c, ov);
             }
-          } else if constexpr (C::kOColsPerWG >= 32) {
+          } else if constexpr (kOColsPerWG >= 32) {
 #pragma unroll
-            for (int c = 0; c < C::kOColsPerWG; c += 32) {
+            for (int c = 0; c < kOColsPerWG; c += 32) {
               uint32_t ov[32];
               tmem_ld32(o_addr + c, ov);
               tmem_wait_ld();
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // an empty key list (possible only through a caller-built CSR; the BlockMask entry
       // points refuse it like attention.cpp:133-136) yields a zero row, never stale TMEM
       const float inv_l = cnt > 0 ? 1.f / l_tot : 0.f;
-      constexpr int kOC = C::kOColsPerWG;
+      constexpr int kOC = kOColsPerWG;
       uint32_t ov[kOC];
       if constexpr (kSplitO) {  // this warpgroup's output columns of both partial rows, merged
         static_assert(kOC == 32, "decoupled epilogue: 32 output columns per warpgroup");
