@@ -503,6 +503,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 64 && s_iter >= C::kSBufs) wait_pv(s_iter - C::kSBufs);
 #endif
         tc_fence_after();
+#ifdef DFS_ATTN_SKIP_SOFTMAX  // experiment builds only (tools/k5_isolation.sh): the MMA/TMA side alone
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_a(p_full0 + sb * 8);
+        ++s_iter;
+        continue;
+#endif
         uint32_t sv[64];
         const int valid = min(kBN, nk32 - vb * kBN) - ch * 64;
         auto load_s = [&]() {
