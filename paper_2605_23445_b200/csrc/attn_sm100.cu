@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY;
       uint64_t lsum[2] = {0, 0};
       int32_t vb_next = vb_first;
+#pragma unroll 2
       for (int32_t j = 0; j < cnt; ++j) {
         const int32_t vb = vb_next;
         if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);
