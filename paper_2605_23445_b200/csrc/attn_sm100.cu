@@ -985,13 +985,13 @@ int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMa
 }
 
 // exp2 split between MUFU and the FMA-pipe polynomial (use_poly), measured with
-// tools/k5_cycles.sh (SM cycles, degree-2 polynomial, row-split kernel): d = 128 runs pairs
-// 1, 4, 7, 10, 13 of every 16 (31 %): HY -4.1 % vs 1, 4, 7 of every 8, -1.2 % vs every 3rd;
-// 0, 3, 6, 9, 12 / 2, 5, 8, 11, 14 of 16 and 4 or 6 of 16 are 2-4 % slower — the placement
-// in the compiler's schedule matters as much as the ratio. d = 64 keeps 1, 4, 7 of every 8
-// (5 of 16 is +3 % there). DFS_ATTN_POLY overrides the default for A/B measurements.
+// tools/poly_sweep.sh (K5 SM cycles, degree-2 polynomial, row-split kernel with the block loop
+// unrolled by 2): d = 128 runs every 3rd pair (33 %): HY -1.8 % vs pairs 1, 4, 7, 10, 13 of 16
+// (which had won by 4 % before the unroll), -2.1 % vs 1, 4, 7 of every 8; d = 64 keeps 1, 4, 7
+// of every 8 (every 3rd +3 %, 5 of 16 +1 %, every 2nd +11 %). The placement in the compiler's
+// schedule matters as much as the ratio. DFS_ATTN_POLY overrides the default for A/B runs.
 template <int D>
-constexpr int kDefaultPoly = D == 128 ? 516 : 38;
+constexpr int kDefaultPoly = D == 128 ? 3 : 38;
 
 template <int D>
 int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
