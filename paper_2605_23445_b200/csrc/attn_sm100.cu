@@ -58,6 +58,18 @@ constexpr uint32_t kTmemCols = 512;
 #define DFS_ATTN_RESCALE_LOG2 8.0f
 #endif
 constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
+// Row split: the rescale test runs on each half-row's block sum of p instead of the max of
+// the exponent arguments (no per-pair max on the ALU pipe): p >= 0, so a sum <= kRescaleSum
+// bounds every p of the block by it; a larger sum sends the block down the rare path, which
+// takes the block's real row max from S (still intact in TMEM).
+#ifndef DFS_ATTN_SUMTEST
+#define DFS_ATTN_SUMTEST 1
+#endif
+constexpr bool kSumTest = DFS_ATTN_SUMTEST;
+#ifndef DFS_ATTN_RESCALE_SUM
+#define DFS_ATTN_RESCALE_SUM 4096.0f
+#endif
+constexpr float kRescaleSum = DFS_ATTN_RESCALE_SUM;
 [[maybe_unused]] constexpr uint32_t kBarRows = 2;  // column split: named barriers 2..5: one per 32-row group (0 = __syncthreads)
 // d = 64: the two softmax warpgroups run DECOUPLED (no per-block row-max exchange): each
 // keeps its own running max / sum for its 64 key columns and its own O accumulator in
@@ -524,13 +536,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         load_s();
         if (tr && hf == 0) trace(p, 12, s_iter);
-        // The running max m is stale by design (O is rescaled only when a block raises it by
-        // more than kRescaleThreshold), so the exponentials of block j need only m, not block
-        // j's own max: they start right after the TMEM load, and the threshold test runs on
-        // their arguments x = s * scale - m (max(x) > threshold), reduced on the ALU pipe inside
-        // the same loop — off the critical path. A block that crosses it (rare: ~0.03 % of
-        // blocks at HY) rescales O and recomputes its exponentials before P is stored. The
-        // first block of a tile sets m from its own max.
+        // The running max m is stale by design (O is rescaled only when a block's p grow too
+        // large), so the exponentials of block j need only m, not block j's own max: they
+        // start right after the TMEM load, and the test runs on their results — each
+        // half-row's block sum of p (kSumTest: sum <= 2^12 bounds every p; costs one FADD2
+        // per block, where the max of the arguments x = s * scale - m cost one FMNMX3 per
+        // pair: HY K5 -3.9 %, C -5.1 % SM cycles) — off the critical path. A block that fails
+        // it (rare) takes its real row max from S, rescales O and recomputes its exponentials
+        // before P is stored. The first block of a tile sets m from its own max.
         if (j == 0) {
           float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -544,12 +557,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto exps = [&]() {
           const uint64_t sc2 = f2_pack(p.scale_log2, p.scale_log2), nm2 = f2_pack(-m, -m);
           lb[0] = lb[1] = 0;
-          float xm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          [[maybe_unused]] float xm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             float x0, x1;
             f2_unpack(f2_fma(f2_pack(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), sc2, nm2), x0, x1);
-            xm[i & 3] = fmaxf(xm[i & 3], fmaxf(x0, x1));
+            if constexpr (!kSumTest) xm[i & 3] = fmaxf(xm[i & 3], fmaxf(x0, x1));
             float p0, p1;
             if (use_poly<POLY>(i)) {
               f2_unpack(ex2_poly2(x0, x1), p0, p1);
@@ -560,12 +573,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             lb[i & 1] = f2_add(lb[i & 1], f2_pack(p0, p1));
             pk[i] = pack_bf16(p0, p1);
           }
-          xmax = fmaxf(fmaxf(xm[0], xm[1]), fmaxf(xm[2], xm[3]));
+          if constexpr (kSumTest) {
+            float a, b;
+            f2_unpack(f2_add(lb[0], lb[1]), a, b);
+            xmax = a + b;  // this half-row's block sum: bounds every p of it (p >= 0)
+          } else {
+            xmax = fmaxf(fmaxf(xm[0], xm[1]), fmaxf(xm[2], xm[3]));
+          }
         };
         exps();
         if (j > 0) {
-          xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, 16));  // the row's other 64 keys
-          if (__any_sync(0xffffffffu, xmax > kRescaleThreshold)) {  // warp-uniform (TMEM ops below)
+          bool big;
+          if constexpr (kSumTest) {
+            big = __any_sync(0xffffffffu, !(xmax <= kRescaleSum));  // also catches inf / NaN sums
+          } else {
+            xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, 16));  // the row's other 64 keys
+            big = __any_sync(0xffffffffu, xmax > kRescaleThreshold);
+          }
+          if (big) {  // warp-uniform (TMEM ops below)
+            if constexpr (kSumTest) {  // rare path: the block's own row max (S_j is intact in TMEM)
+              load_s();
+              float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+              for (int i = 0; i < 64; ++i) mq[i & 3] = fmaxf(mq[i & 3], __uint_as_float(sv[i]));
+              const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+              xmax = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * p.scale_log2 - m;
+            }
             const float m_new = m + fmaxf(xmax, 0.f);
             wait_pv(s_iter - 1);  // PV_{j-1} complete: O stable
             tc_fence_after();

@@ -188,15 +188,17 @@ def test_fuzz_tcgen05_vs_fp32_torch_reference():
             assert err <= 2e-2, (trial, name, n, h, d, k, gather, err)
 
 
-@pytest.mark.parametrize("jump", [0.5, 40.0, 400.0])
-def test_logit_jump_across_blocks(jump):
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("jump", [0.5, 6.0, 12.0, 40.0, 400.0])
+def test_logit_jump_across_blocks(jump, d):
     """Online-softmax rescaling under large row-max jumps: key block 3 carries logits
     `jump` log2 units above block 0's (400 would overflow fp32 without the O/l rescale,
-    0.5 stays under the lazy-rescale threshold). Output must match a torch fp32 softmax,
-    and a following ordinary call must be unaffected."""
+    0.5 and 6 stay under the lazy-rescale test — a half-row's block sum of p <= 2^12 —
+    12 crosses it). Output must match a torch fp32 softmax, and a following ordinary call
+    must be unaffected."""
     m = dfs()
     gen = torch.Generator().manual_seed(7)
-    h, n, d = 2, 1024 + 40, 128
+    h, n = 2, 1024 + 40
     q = torch.full((h, n, d), 1.0) + 0.05 * torch.randn(h, n, d, generator=gen)
     kk = 0.05 * torch.randn(h, n, d, generator=gen)
     # logit_log2 = q.k / sqrt(d) * log2(e): choose block 3's key scale for the requested jump
