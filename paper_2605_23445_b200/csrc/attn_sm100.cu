@@ -57,7 +57,7 @@ constexpr uint32_t kTmemCols = 512;
 #ifndef DFS_ATTN_RESCALE_LOG2
 #define DFS_ATTN_RESCALE_LOG2 8.0f
 #endif
-constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
+[[maybe_unused]] constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
 // Row split: the rescale test runs on each half-row's block sum of p instead of the max of
 // the exponent arguments (no per-pair max on the ALU pipe): p >= 0, so a sum <= kRescaleSum
 // bounds every p of the block by it; a larger sum sends the block down the rare path, which
@@ -66,6 +66,11 @@ constexpr float kRescaleThreshold = DFS_ATTN_RESCALE_LOG2;  // log2 units
 #define DFS_ATTN_SUMTEST 1
 #endif
 constexpr bool kSumTest = DFS_ATTN_SUMTEST;
+// row split: S_j read from TMEM as one x64 load per thread, or as 2 / 4 smaller loads
+#ifndef DFS_ATTN_LDSPLIT
+#define DFS_ATTN_LDSPLIT 2
+#endif
+constexpr int kLdSplit = DFS_ATTN_LDSPLIT;
 #ifndef DFS_ATTN_RESCALE_SUM
 #define DFS_ATTN_RESCALE_SUM 4096.0f
 #endif
@@ -195,6 +200,10 @@ __device__ __forceinline__ constexpr bool use_poly(int i) {
     return (0x92u >> (i % 8)) & 1u;  // pairs 1, 4, 7 of each 8
   } else if constexpr (POLY == 516) {
     return (0x2492u >> (i % 16)) & 1u;  // pairs 1, 4, 7, 10, 13 of each 16
+  } else if constexpr (POLY >= 100 && POLY < 132) {
+    return i >= POLY - 100;  // the row slice's last pairs (MUFU pairs first in the schedule)
+  } else if constexpr (POLY == 201) {
+    return i >= 16 && i % 3 != 0;  // 11 pairs, all in the second half of the slice
   } else {
     return i % POLY == POLY - 1;
   }
@@ -526,7 +535,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t sv[64];
         const int valid = min(kBN, nk32 - vb * kBN) - ch * 64;
         auto load_s = [&]() {
-          tmem_ld16x2_x64<64>(tmem + lane_addr + sb * 128, sv);
+          if constexpr (kLdSplit == 4) {  // four x16 loads: each chunk's consumers wait only for their own
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld16x2_x16<64>(tmem + lane_addr + sb * 128 + c * 16, sv + c * 16);
+          } else if constexpr (kLdSplit == 2) {
+            tmem_ld16x2_x32<64>(tmem + lane_addr + sb * 128, *reinterpret_cast<uint32_t(*)[32]>(sv));
+            tmem_ld16x2_x32<64>(tmem + lane_addr + sb * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+          } else {
+            tmem_ld16x2_x64<64>(tmem + lane_addr + sb * 128, sv);
+          }
           tmem_wait_ld();
           if (valid < 64) {  // padded keys of a partial last block (attention.cpp:146-152)
 #pragma unroll
@@ -1070,6 +1087,13 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
       case 3: rc = launch_kernel<D, 3>(mq, mk, mv, p, stream); break;
       case 38: rc = launch_kernel<D, 38>(mq, mk, mv, p, stream); break;
       case 516: rc = launch_kernel<D, 516>(mq, mk, mv, p, stream); break;
+#ifdef DFS_ATTN_POLY_EXTRA
+      case 120: rc = launch_kernel<D, 120>(mq, mk, mv, p, stream); break;
+      case 121: rc = launch_kernel<D, 121>(mq, mk, mv, p, stream); break;
+      case 122: rc = launch_kernel<D, 122>(mq, mk, mv, p, stream); break;
+      case 118: rc = launch_kernel<D, 118>(mq, mk, mv, p, stream); break;
+      case 201: rc = launch_kernel<D, 201>(mq, mk, mv, p, stream); break;
+#endif
       default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
     }
   }
