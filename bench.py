@@ -666,7 +666,8 @@ def main():
                    "sub_block": Bs, "gamma": gamma, "K": K, "M": m, "parallelism": ((f"ulysses NCCL all-to-all x{world}" if args.ulysses_nccl else
                                     f"ulysses all-to-all fused into K2/K5 (P2P) x{world}") if ulysses_mode
                                    else f"head-shard x{world}"),
-                   "l2": "inputs 3x730 MB bf16 > 126 MB L2 (no flush needed)"},
+                   "l2": (f"q/k/v/o {n * hl * d * 2 / 1e6:.0f} MB bf16 each, {4 * n * hl * d * 2 / 1e6:.0f} MB touched "
+                          f"per step + the permuted K/V copies > 126 MB L2 (no flush between steps)")},
         "ms_per_call_mask_reuse": t_reuse,
         "order_K1_ms_per_geometry": t_k1,
         "lut_overlap": overlap,

@@ -44,6 +44,16 @@ constexpr int kSoftThreads = 128 * kSWG;
 constexpr int kThreads = 64 + kSoftThreads;
 constexpr float kLoScale = 2048.f;        // 2^11
 constexpr float kInvLoScale = 1.f / 2048.f;
+// Lazy row max (as in K5): a slice's running max m is set from its first key tile and then
+// kept while the tile sums of 2^(l - m) stay <= kLazySum (every p of the tile is bounded by
+// its sum); the exponent arguments come straight out of the logit FMAs and no per-tile max
+// is computed. A tile whose sum exceeds it (rare) raises m to its own max and recomputes.
+// The scratch stores the m each tile used, so the fix-up is unchanged.
+#ifndef DFS_SCORE_LAZY
+#define DFS_SCORE_LAZY 0
+#endif
+constexpr bool kLazy = DFS_SCORE_LAZY;
+constexpr float kLazySum = 65536.f;
 
 // CTA pairs (cta_group::2): the pair's MMA is M = 256 (each CTA's own 128-row stripe)
 // x N = 128 keys, and each CTA holds only half of every key tile (64 keys) — the pooled
@@ -282,6 +292,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // logits l = (D1 + D2 / 2^11) * f in packed fp32x2 arithmetic; only the tile holding
         // the end of the valid pooled keys masks (warp-uniform branch)
         uint64_t l2[16];
+        // kLazy: x = l - m straight from the FMAs (m of the first tile: 0 here, set below)
+        const bool lazy = kLazy && kt > 0;
+        const uint64_t nm2 = f2_pack(lazy ? -m : 0.f, lazy ? -m : 0.f);
         {
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
@@ -291,8 +304,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-              l2[c * 8 + i] = f2_fma(f2_pack(__uint_as_float(a2[2 * i]), __uint_as_float(a2[2 * i + 1])), g2,
-                                     f2_mul(f2_pack(__uint_as_float(a1[2 * i]), __uint_as_float(a1[2 * i + 1])), f2));
+              l2[c * 8 + i] = kLazy ? f2_fma(f2_pack(__uint_as_float(a2[2 * i]), __uint_as_float(a2[2 * i + 1])), g2,
+                                             f2_fma(f2_pack(__uint_as_float(a1[2 * i]), __uint_as_float(a1[2 * i + 1])), f2, nm2))
+                                    : f2_fma(f2_pack(__uint_as_float(a2[2 * i]), __uint_as_float(a2[2 * i + 1])), g2,
+                                             f2_mul(f2_pack(__uint_as_float(a1[2 * i]), __uint_as_float(a1[2 * i + 1])), f2));
           }
         }
         tc_fence_before();
@@ -310,6 +325,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             l2[i] = f2_pack(x0, x1);
           }
         }
+        float tg[G];
+        if (lazy) {  // l2 holds x = l - m
+          auto sums = [&](float shift) {  // tile sums of 2^(x - shift)
+            const uint64_t sh2 = f2_pack(-shift, -shift);
+            float s = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              uint64_t t2 = 0;
+#pragma unroll
+              for (int i = 0; i < SUBS / 2; ++i) {
+                float x0, x1;
+                f2_unpack(shift != 0.f ? f2_add(l2[g * (SUBS / 2) + i], sh2) : l2[g * (SUBS / 2) + i], x0, x1);
+                t2 = f2_add(t2, f2_pack(ex2(x0), ex2(x1)));
+              }
+              float ta, tb;
+              f2_unpack(t2, ta, tb);
+              tg[g] = ta + tb;
+              s += tg[g];
+            }
+            return s;
+          };
+          float s = sums(0.f);
+          if (__any_sync(0xffffffffu, !(s <= kLazySum))) {  // rare: raise m to this tile's max
+            float mx = -INFINITY;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float x0, x1;
+              f2_unpack(l2[i], x0, x1);
+              mx = fmaxf(mx, fmaxf(x0, x1));
+            }
+            if (mx > 0.f) {
+              s = sums(mx);
+              z *= ex2(-mx);
+              m += mx;
+            }
+          }
+          z += s;
+        } else {
         float mx = -INFINITY;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -318,7 +371,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mx = fmaxf(mx, fmaxf(x0, x1));
         }
         const float mn = fmaxf(m, mx);
-        float tg[G];
         if (mn > -INFINITY) {
           const uint64_t nm2 = f2_pack(-mn, -mn);
           float s = 0.f;
@@ -341,6 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         } else {
 #pragma unroll
           for (int g = 0; g < G; ++g) tg[g] = 0.f;
+        }
         }
         if (prev.valid) fix_tile(kt, t_old, mu_old);
         // coalesced across the warp: 32 consecutive rows per (v) / (kt, slice) entry
