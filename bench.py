@@ -519,6 +519,32 @@ def main():
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
 
+    # ---- the same call under CUPTI (torch.profiler, after the timed region): per-kernel
+    # durations inside the update-step call, grouped by stage (the CUDA-event decomposition
+    # below times each stage alone, so its clocks can differ from the step's)
+    step_kernels = None
+    if not ulysses_mode:
+        try:
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                for _ in range(3):
+                    step()
+                torch.cuda.synchronize()
+            stages = {"K2_permute_pool": ("permute_kernel", "Memset"), "K3_score": ("absmax", "split_kernel", "score_"),
+                      "K4_topk": ("topk", "lut_ptr"), "K5_attn": ("attn_",)}
+            acc = {k: 0.0 for k in stages}
+            acc["other"] = 0.0
+            evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+            for e in evs:
+                dur = (e.time_range.end - e.time_range.start) / 1e3 / 3
+                key = next((k for k, pats in stages.items() if any(pt in e.name for pt in pats)), "other")
+                acc[key] += dur
+            span = (max(e.time_range.end for e in evs) - min(e.time_range.start for e in evs)) / 1e3 / 3
+            step_kernels = {k: round(v, 4) for k, v in acc.items()}
+            step_kernels["span_per_call"] = round(span, 4)
+        except Exception as ex:  # pragma: no cover
+            step_kernels = {"failed": str(ex)}
+
     # ---- decomposition (per-kernel CUDA-event timing on the launching stream) ---
     # the same kernels run_step launches: K2 read-only pooling of q and k in Hilbert order,
     # K3, K4, and K5 gathering the Hilbert-ordered rows itself (fused reorder + unpermute)
@@ -673,6 +699,7 @@ def main():
         "lut_overlap": overlap,
         "executed_tflop_per_call": exec_flops / 1e12, "dense_equiv_tflop_per_call": dense_flops / 1e12,
         "executed_tflops": exec_flops / (ms_max * 1e-3) / 1e12,
+        "step_kernel_ms_cupti": step_kernels,
         "breakdown_ms": {"reorder_pool_K2": t_perm, "score_K3": t_score, "topk_K4": t_topk,
                          "attn_unpermute_K5": t_attn},
         "gpu_launches": launches_per_step * args.steps,

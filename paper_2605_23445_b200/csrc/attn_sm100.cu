@@ -511,7 +511,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY;
       uint64_t lsum[2] = {0, 0};
       int32_t vb_next = vb_first;
+#ifdef DFS_SYNCCHECK_BUILD
+  // Unrolled, ptxas addresses the second copy's S wait as [o_done register - 0x30]: the
+  // right barrier (checked in the SASS), but compute-sanitizer synccheck reports every such
+  // wait as "missing init"; the sanitizer build keeps the loop rolled (same protocol).
+#pragma unroll 1
+#else
 #pragma unroll 2
+#endif
       for (int32_t j = 0; j < cnt; ++j) {
         const int32_t vb = vb_next;
         if (j + 1 < cnt) vb_next = block_at(p, beg, j + 1);

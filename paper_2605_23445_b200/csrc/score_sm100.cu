@@ -50,7 +50,7 @@ constexpr float kInvLoScale = 1.f / 2048.f;
 // is computed. A tile whose sum exceeds it (rare) raises m to its own max and recomputes.
 // The scratch stores the m each tile used, so the fix-up is unchanged.
 #ifndef DFS_SCORE_LAZY
-#define DFS_SCORE_LAZY 0
+#define DFS_SCORE_LAZY 1
 #endif
 constexpr bool kLazy = DFS_SCORE_LAZY;
 constexpr float kLazySum = 65536.f;
