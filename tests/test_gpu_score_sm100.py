@@ -146,3 +146,29 @@ def test_topk_tie_heavy_fuzz_bit_exact():
                 got[np.arange(mm)[:, None], lut] = True
                 want = mask_bits_to_dense(ora.topk_select(S, gam), mm)
                 assert (got == want).all(), (mm, kind, gam)
+
+
+@pytest.mark.parametrize("jump", [4.0, 20.0, 60.0])
+def test_scores_under_logit_jumps_across_key_tiles(jump):
+    """The scorer's lazy row max (score_sm100.cu kLazy): a slice keeps the first key tile's max
+    while its tile sums stay <= 2^16, and a later tile whose pooled logits jump by `jump` log2
+    units (20 and 60 cross the test, 4 does not) raises it. Scores must still match the fp64
+    oracle within 1e-4 and select the same masks."""
+    rng = np.random.default_rng(11)
+    n, d, b, bs = 8192, 128, 128, 16
+    q = bf16_round((1.0 + 0.1 * rng.standard_normal((n, d))).astype(np.float32))
+    k = 0.1 * rng.standard_normal((n, d)).astype(np.float32)
+    # pooled logit of key tile 2 (pooled keys 256..383 = tokens 4096..6143) raised by `jump` log2 units
+    c = jump / (d / d ** 0.5 * 1.4426950408889634)
+    k[4096:6144] += c
+    k = bf16_round(k)
+    S = gpu_scores([q, q], [k, k], b, bs)
+    ref = ora.block_scores(q, k, b, bs)
+    for h in range(2):
+        err = np.abs(S[h] - ref).max() / np.abs(ref).max()
+        assert err <= 1e-4, (jump, h, err)
+        mm = ref.shape[0]
+        for gam in (0.1, 0.25):
+            want = mask_bits_to_dense(ora.topk_select(ref, gam), mm)
+            got = mask_bits_to_dense(ora.topk_select(S[h], gam), mm)
+            assert (want == got).mean() >= 0.995, (jump, gam, h)
