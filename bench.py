@@ -69,6 +69,7 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.power = []  # W
         self.stop = threading.Event()
         self.proc = None
         self.thread = None
@@ -81,6 +82,10 @@ class ClockSampler:
         while not self.stop.is_set():
             try:
                 self.sm.append(float(nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)))
+                try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(hdl) / 1000.0)
+                except Exception:
+                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(hdl)
                 self.reasons.update(name for bit, name in bits.items() if r & bit)
             except Exception:
@@ -119,6 +124,7 @@ class ClockSampler:
                 try:
                     self.sm.append(float(parts[0]))
                     self.max_mhz = float(parts[1])
+                    self.power.append(float(parts[2]))
                 except ValueError:
                     continue
                 self.reasons.update(self.NAMES[i] for i in range(4) if parts[3 + i].lower() == "active")
@@ -137,8 +143,11 @@ class ClockSampler:
     def summary(self):
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm)}
+        out = {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "samples": len(self.sm)}
+        if self.power:
+            out["power_w"] = round(statistics.median(self.power), 1)
+        return out
 
 
 def smooth_fields(dims, heads, d, seed, device, rounds=4):
