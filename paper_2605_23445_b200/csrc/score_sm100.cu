@@ -54,6 +54,12 @@ constexpr float kInvLoScale = 1.f / 2048.f;
 #endif
 constexpr bool kLazy = DFS_SCORE_LAZY;
 constexpr float kLazySum = 65536.f;
+// every kPolyEvery-th exponential pair of the lazy path on the FMA-pipe degree-5 polynomial
+// (fp32-accurate, sm100.cuh ex2_poly5x2); 0 = all on MUFU
+#ifndef DFS_SCORE_POLY
+#define DFS_SCORE_POLY 4
+#endif
+constexpr int kPolyEvery = DFS_SCORE_POLY;
 
 // CTA pairs (cta_group::2): the pair's MMA is M = 256 (each CTA's own 128-row stripe)
 // x N = 128 keys, and each CTA holds only half of every key tile (64 keys) — the pooled
@@ -337,7 +343,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int i = 0; i < SUBS / 2; ++i) {
                 float x0, x1;
                 f2_unpack(shift != 0.f ? f2_add(l2[g * (SUBS / 2) + i], sh2) : l2[g * (SUBS / 2) + i], x0, x1);
-                t2 = f2_add(t2, f2_pack(ex2(x0), ex2(x1)));
+                if (kPolyEvery && (g * (SUBS / 2) + i) % kPolyEvery == kPolyEvery - 1)
+                  t2 = f2_add(t2, ex2_poly5x2(x0, x1));  // FMA pipe (offloads MUFU)
+                else
+                  t2 = f2_add(t2, f2_pack(ex2(x0), ex2(x1)));
               }
               float ta, tb;
               f2_unpack(t2, ta, tb);

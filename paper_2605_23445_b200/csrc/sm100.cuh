@@ -474,6 +474,30 @@ __device__ __forceinline__ uint64_t ex2_poly2(float x0, float x1) {
                  __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
 }
 
+// fp32-accurate 2^x on the FMA pipe for a pair (the scorer's exponentials, which feed fp64
+// block scores and the top-K cut): the same round-split and exponent insertion as
+// ex2_poly2, degree-5 near-minimax polynomial on [-0.5, 0.5] (max relative error 2.3e-7 in
+// fp32 Horner evaluation, the same order as ex2.approx.ftz.f32). x >= -125 after the clamp.
+__device__ __forceinline__ uint64_t ex2_poly5x2(float x0, float x1) {
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  const uint64_t x = f2_pack(x0, x1);
+  const uint64_t t = f2_add(x, f2_pack(12582912.f, 12582912.f));
+  const uint64_t nf = f2_add(t, f2_pack(-12582912.f, -12582912.f));
+  const uint64_t f = f2_fma(nf, f2_pack(-1.f, -1.f), x);
+  uint64_t p = f2_fma(f2_pack(0.001327647129073739f, 0.001327647129073739f), f,
+                      f2_pack(0.009675540961325169f, 0.009675540961325169f));
+  p = f2_fma(p, f, f2_pack(0.05550713092088699f, 0.05550713092088699f));
+  p = f2_fma(p, f, f2_pack(0.24022120237350464f, 0.24022120237350464f));
+  p = f2_fma(p, f, f2_pack(0.6931469440460205f, 0.6931469440460205f));
+  p = f2_fma(p, f, f2_pack(1.0000001192092896f, 1.0000001192092896f));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  return f2_pack(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+                 __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
