@@ -57,7 +57,7 @@ constexpr float kLazySum = 65536.f;
 // every kPolyEvery-th exponential pair of the lazy path on the FMA-pipe degree-5 polynomial
 // (fp32-accurate, sm100.cuh ex2_poly5x2); 0 = all on MUFU
 #ifndef DFS_SCORE_POLY
-#define DFS_SCORE_POLY 4
+#define DFS_SCORE_POLY 6
 #endif
 constexpr int kPolyEvery = DFS_SCORE_POLY;
 
