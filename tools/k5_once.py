@@ -6,6 +6,8 @@ from paper_2605_23445_b200 import ops
 from bench import WORKLOADS, smooth_fields
 wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else 'HY']
 dims, H, d, B, Bs, g = wl["dims"], wl["heads"], wl["d"], wl["block"], wl["sub"], wl["gamma"]
+import os
+g = float(os.environ.get("K5_GAMMA", g))  # override the workload's kept fraction
 n = dims[0] * dims[1] * dims[2]; m = -(-n // B)
 q, k, v = smooth_fields(dims, H, d, 1, torch.device("cuda"))
 perm = dfs.hilbert3d_order(dims)
