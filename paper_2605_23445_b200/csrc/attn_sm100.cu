@@ -200,10 +200,6 @@ __device__ __forceinline__ constexpr bool use_poly(int i) {
     return (0x92u >> (i % 8)) & 1u;  // pairs 1, 4, 7 of each 8
   } else if constexpr (POLY == 516) {
     return (0x2492u >> (i % 16)) & 1u;  // pairs 1, 4, 7, 10, 13 of each 16
-  } else if constexpr (POLY >= 100 && POLY < 132) {
-    return i >= POLY - 100;  // the row slice's last pairs (MUFU pairs first in the schedule)
-  } else if constexpr (POLY == 201) {
-    return i >= 16 && i % 3 != 0;  // 11 pairs, all in the second half of the slice
   } else {
     return i % POLY == POLY - 1;
   }
@@ -1094,13 +1090,6 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
       case 3: rc = launch_kernel<D, 3>(mq, mk, mv, p, stream); break;
       case 38: rc = launch_kernel<D, 38>(mq, mk, mv, p, stream); break;
       case 516: rc = launch_kernel<D, 516>(mq, mk, mv, p, stream); break;
-#ifdef DFS_ATTN_POLY_EXTRA
-      case 120: rc = launch_kernel<D, 120>(mq, mk, mv, p, stream); break;
-      case 121: rc = launch_kernel<D, 121>(mq, mk, mv, p, stream); break;
-      case 122: rc = launch_kernel<D, 122>(mq, mk, mv, p, stream); break;
-      case 118: rc = launch_kernel<D, 118>(mq, mk, mv, p, stream); break;
-      case 201: rc = launch_kernel<D, 201>(mq, mk, mv, p, stream); break;
-#endif
       default: rc = launch_kernel<D, 4>(mq, mk, mv, p, stream); break;
     }
   }

@@ -1,4 +1,5 @@
-# exp2 split placement sweep on a library built with -DDFS_ATTN_POLY_EXTRA (build/ab/lib_pext.so)
+# exp2 split placement sweep (round 2; the back-placed POLY codes 118-122 and 201 it measured were
+# removed from attn_sm100.cu after it, see DESIGN §3 and profiles/r2/poly_placement_sweep.txt)
 OUT=gpurun_out/${1:-poly2}; mkdir -p $OUT
 export DFS_B200_LIB=build/ab/lib_pext.so
 for pp in 3 121 120 122 118 201; do DFS_ATTN_POLY=$pp bash tools/k5_cycles.sh "" HY_$pp HY >> $OUT/cycles.txt 2>&1; done
