@@ -163,3 +163,29 @@ def test_two_processes_on_one_gpu(mode, tmp_path):
         assert torch.equal(masks, torch.stack(want_masks))
     else:
         assert torch.equal(torch.cat(outs, 0), want.cpu())
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's multi-rank path as the driver's scaling run uses it (`bench.py --gpus N`
+    relaunching itself under torch.distributed.run), here with two ranks sharing one B200
+    (DFS_BENCH_RANKS_PER_GPU=2, gloo): one JSON line from rank 0 with n_gpus = 2, each rank
+    holding half of the heads, a positive whole-job value, e2e and the CUPTI stage split."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DFS_BENCH_RANKS_PER_GPU="2")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "C", "--steps",
+                        "3", "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True, timeout=900,
+                       env=env, cwd=root)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["heads_per_gpu"] == 24, d["config"]
+    assert d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert d["step_kernel_ms_cupti"] and "failed" not in d["step_kernel_ms_cupti"], d["step_kernel_ms_cupti"]
