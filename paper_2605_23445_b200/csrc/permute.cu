@@ -15,6 +15,13 @@
 
 #include "common.cuh"
 
+#ifndef DFS_PERMUTE_BATCH
+#define DFS_PERMUTE_BATCH 8  // independent 16-byte row loads in flight per thread
+#endif
+#ifndef DFS_PERMUTE_CTA
+#define DFS_PERMUTE_CTA 128  // most (head, 16-byte chunk) slots per CTA before splitting over blockIdx.y
+#endif
+
 namespace dfsgpu {
 
 namespace {
@@ -63,12 +70,12 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
                                                       int32_t* __restrict__ nonfinite,
                                                       const dfs_peer_table* __restrict__ peers = nullptr) {
   constexpr int V = Vec<T>::N;
-  // independent 16-byte row loads in flight per thread: 4 keeps the pooling variant at
-  // <= 56 registers (3 CTAs of 384 threads per SM); 8 or 16 cost more in occupancy than
-  // they gain in memory-level parallelism (tools/permute_bench.py: 0.73 -> 0.69 ms at HY)
-  // (r2: 8 in flight for the pooling variants measured again — q pass 0.191 -> 0.213 ms, k pass
-  // 0.267 -> 0.284 ms at HY, tools/permute_bench.py — so 4 stays)
-  constexpr int kBatch = 4;
+  // independent 16-byte row loads in flight per thread, with the (head, chunk) slots split
+  // over 128-thread CTAs (DFS_PERMUTE_CTA): more, smaller CTAs per SM and 8 loads each beat
+  // 384-thread CTAs with 4 (round 2, tools/permute_bench.py: HY 0.693 -> 0.647 ms for the three
+  // passes, W4 0.342 -> 0.311, C 0.131 -> 0.120; 16 in flight: 0.911; 384-thread CTAs with 8
+  // in flight had lost to occupancy in round 1)
+  constexpr int kBatch = kPeer ? 4 : DFS_PERMUTE_BATCH;  // the peer-pointer variant spills at 8
   const int64_t vec_per_row = d / V;
   const int64_t slots = heads * vec_per_row;
   const int64_t r0 = int64_t(blockIdx.x) * rows;
@@ -93,8 +100,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(const T* __restrict__ src
   }
   __syncthreads();
   bool bad = false;
-  // slots split over blockIdx.y when one CTA would need more than 384 threads (keeps 3 CTAs
-  // of the pooling variant resident per SM; 40 heads x 16 chunks = 640 slots -> 2 x 320)
+  // slots split over blockIdx.y when one CTA would need more than DFS_PERMUTE_CTA threads
+  // (HY: 24 heads x 16 chunks = 384 slots -> 3 x 128)
   for (int64_t s = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; s < slots; s += int64_t(gridDim.y) * blockDim.x) {
     const int64_t h = s / vec_per_row;
     const int64_t c = (s % vec_per_row) * V;
@@ -193,7 +200,7 @@ int launch(const void* src, int src_layout, void* dst, int dst_layout, const uin
     // one thread per (head, 16-byte column chunk) slot when that fits a CTA: every thread
     // then walks the CTA's rows once (no second round for a remainder of slots)
     const int64_t slots = heads * (d / Vec<T>::N);
-    const int64_t ysplit = ceil_div(slots, 384);
+    const int64_t ysplit = ceil_div(slots, int64_t(DFS_PERMUTE_CTA));
     const int threads = int(ceil_div(ceil_div(slots, ysplit), 32) * 32);
     const dim3 g{unsigned(grid), unsigned(ysplit), 1u};
     if (ysplit > 65535) return fail(DFS_E_UNSUPPORTED, "permute: rows too wide");
@@ -401,7 +408,7 @@ int permute_rows_peer_impl(const dfs_peer_table* peers_dev, int64_t heads_total,
   const int64_t rows = pooled ? pool : 16;
   const int64_t grid = ceil_div(n, rows);
   const int64_t slots = heads * (d / 8);
-  const int64_t ysplit = ceil_div(slots, 384);
+  const int64_t ysplit = ceil_div(slots, int64_t(DFS_PERMUTE_CTA));
   const int threads = int(ceil_div(ceil_div(slots, ysplit), 32) * 32);
   if (grid > int64_t(INT32_MAX) || ysplit > 65535) return fail(DFS_E_UNSUPPORTED, "alltoall: too many rows");
   (void)heads_total;
