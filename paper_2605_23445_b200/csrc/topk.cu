@@ -162,9 +162,23 @@ __global__ void __launch_bounds__(128) topk_warp_kernel(const double* __restrict
   uint32_t hi[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) hi[c] = uint32_t(key[c] >> 32);
-  uint32_t t_hi = 0;
+  // T lies between the smallest and the largest real key, so it shares every high bit above
+  // the highest bit in which those two differ: start the bisection below that bit (block
+  // scores are probabilities — sign and most exponent bits are common to a whole row)
+  uint32_t hmin = 0xffffffffu, hmax = 0u;
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+    if (c * 32 + lane < m) {
+      hmin = min(hmin, hi[c]);
+      hmax = max(hmax, hi[c]);
+    }
+  hmin = __reduce_min_sync(0xffffffffu, hmin);
+  hmax = __reduce_max_sync(0xffffffffu, hmax);
+  const uint32_t diff = hmin ^ hmax;
+  const int top = diff ? 31 - __clz(diff) : -1;  // highest differing bit (-1: all high words equal)
+  uint32_t t_hi = top < 0 ? hmin : top >= 31 ? 0u : hmin & ~((2u << top) - 1u);
   bool exact = false;
-  for (int bit = 31; bit >= 0; --bit) {
+  for (int bit = top; bit >= 0; --bit) {
     const uint32_t cand = t_hi | (1u << bit);
     int c = 0;
 #pragma unroll
