@@ -164,7 +164,7 @@ struct TileMeta {
 };
 __device__ __forceinline__ TileMeta load_meta(const Params& p, int64_t tile) {
   TileMeta t{0, 0};
-  if (tile < p.tiles) {
+  if (tile >= 0 && tile < p.tiles) {
     if (p.blk_ptr) {
       t.beg = __ldg(p.blk_ptr + tile);
       t.cnt = __ldg(p.blk_ptr + tile + 1) - t.beg;
@@ -173,6 +173,27 @@ __device__ __forceinline__ TileMeta load_meta(const Params& p, int64_t tile) {
     }
   }
   return t;
+}
+
+// The it-th tile of this CTA (-1: done). kMcast (dense steps, 2-CTA clusters): the two CTAs
+// of a cluster take query blocks (2v, 2v+1) of one head, which walk the same key blocks, so
+// the even CTA multicasts every K/V tile into both; with an odd block count the odd CTA
+// repeats the head's last block without storing it (a "phantom" tile).
+template <bool kMcast>
+__device__ __forceinline__ int64_t tile_at(const Params& p, int64_t it) {
+  if constexpr (!kMcast) {
+    const int64_t t = int64_t(blockIdx.x) + it * gridDim.x;
+    return t < p.tiles ? t : -1;
+  } else {
+    const int64_t pph = (p.mq + 1) / 2, pi = int64_t(blockIdx.x >> 1) + it * (gridDim.x >> 1);
+    if (pi >= p.heads * pph) return -1;
+    const int64_t u = 2 * (pi % pph) + (blockIdx.x & 1);
+    return (pi / pph) * p.mq + (u < p.mq ? u : p.mq - 1);
+  }
+}
+template <bool kMcast>
+__device__ __forceinline__ bool phantom_tile(const Params& p, int64_t tile) {
+  return kMcast && (blockIdx.x & 1) && (p.mq & 1) && tile % p.mq == p.mq - 1;
 }
 
 #ifndef DFS_TRACE_T0
@@ -205,7 +226,7 @@ __device__ __forceinline__ constexpr bool use_poly(int i) {
   }
 }
 
-template <int D, int POLY, bool kPeerOut>
+template <int D, int POLY, bool kPeerOut, bool kMcast>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, const Params p) {
@@ -236,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(&bars->kv_full[i], 1);
-      mbar_init(&bars->kv_empty[i], 1);
+      mbar_init(&bars->kv_empty[i], kMcast ? 2 : 1);  // kMcast: both CTAs' MMAs release a slot
     }
     fence_barrier_init();
   }
@@ -249,6 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (kMcast) cluster_sync();  // the peer's barriers are initialised before any remote arrival
   const uint32_t tmem = bars->tmem_base;
 
   if (warp == 0) {
@@ -303,15 +325,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (elect_one()) mbar_arrive(&bars->kv_full[slot]);
       __syncwarp();
 #else
-      issue_tile(map, h, row0, sRing + slot * C::kTileBytes, &bars->kv_full[slot], rr, false);
+      if constexpr (kMcast) {  // each CTA expects the bytes; the even CTA multicasts them into both
+        if (elect_one()) {
+          mbar_expect_tx(&bars->kv_full[slot], C::kTileBytes);
+          if ((blockIdx.x & 1) == 0) {
+#pragma unroll
+            for (int c = 0; c < C::kChunks; ++c)
+              tma_load_3d_mcast2(sRing + slot * C::kTileBytes + c * C::kChunkBytes, map, &bars->kv_full[slot], c * 64,
+                                 p.in_nhd ? int(h) : int(row0), p.in_nhd ? int(row0) : int(h));
+          }
+        }
+        __syncwarp();
+      } else {
+        issue_tile(map, h, row0, sRing + slot * C::kTileBytes, &bars->kv_full[slot], rr, false);
+      }
 #endif
       ++ring;
     };
-    TileMeta nxt = load_meta(p, blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+    TileMeta nxt = load_meta(p, tile_at<kMcast>(p, 0));
+    for (int64_t it = 0, tile = tile_at<kMcast>(p, 0); tile >= 0; tile = tile_at<kMcast>(p, ++it)) {
       const int64_t h = tile / p.mq, u = tile % p.mq;
       const int32_t beg = nxt.beg, cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta(p, tile_at<kMcast>(p, it + 1));
       {
         int rr[4] = {0, 0, 0, 0};
         if (p.in_rows) gather_rows(h, u * kBM, rr);  // row indices fetched while Q's slot drains
@@ -385,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_ss(tmem + sb * 128, q_lo + off, kHiK, k_lo + off, kHiK, C::kIdescQK, s > 0);
 #endif
         }
-        umma_commit(&bars->kv_empty[slot]);
+        if constexpr (kMcast) umma_commit_both(&bars->kv_empty[slot]); else umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->s_full[sb]);
       }
       __syncwarp();
@@ -411,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
         if (elect_one()) {
-          umma_commit(&bars->kv_empty[slot]);
+          if constexpr (kMcast) umma_commit_both(&bars->kv_empty[slot]); else umma_commit(&bars->kv_empty[slot]);
           umma_commit(&bars->o_done[pb]);
         }
         __syncwarp();
@@ -432,17 +467,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                   (!first || s > 0) ? 1u : 0u);
 #endif
         }
-        umma_commit(&bars->kv_empty[slot]);
+        if constexpr (kMcast) umma_commit_both(&bars->kv_empty[slot]); else umma_commit(&bars->kv_empty[slot]);
         umma_commit(&bars->o_done[pb]);
       }
       __syncwarp();
       trace(p, 16, pv_iter);
       ++pv_iter;
     };
-    TileMeta nxt = load_meta(p, blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+    TileMeta nxt = load_meta(p, tile_at<kMcast>(p, 0));
+    for (int64_t it = 0, tile = tile_at<kMcast>(p, 0); tile >= 0; tile = tile_at<kMcast>(p, ++it)) {
       const int32_t cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta(p, tile_at<kMcast>(p, it + 1));
       mbar_wait(&bars->q_full, q_phase);
       q_phase ^= 1;
       auto release_q = [&]() {  // Q smem free once the last QK read it (kQT: once copied to TMEM)
@@ -496,12 +531,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                   "barrier layout");
     auto wait_pv = [&](uint32_t g) { mbar_wait_a(o_done0 + (g % C::kSBufs) * 8, (g / C::kSBufs) & 1); };
     const int32_t nk32 = int32_t(p.nk);
-    TileMeta nxt = load_meta(p, blockIdx.x);
+    TileMeta nxt = load_meta(p, tile_at<kMcast>(p, 0));
     int32_t vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
-    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+    for (int64_t it = 0, tile = tile_at<kMcast>(p, 0); tile >= 0; tile = tile_at<kMcast>(p, ++it)) {
       const int64_t h = tile / p.mq, u = tile % p.mq;
       const int32_t beg = nxt.beg, cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta(p, tile_at<kMcast>(p, it + 1));
       const int64_t i_row = u * kBM + r;
       const int64_t orow = i_row < p.nq && p.out_rows ? int64_t(__ldg(p.out_rows + i_row)) : i_row;
       float m = -INFINITY;
@@ -673,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16x2_x32<32>(tmem + lane_addr + C::kOCol, ov);
       tmem_wait_ld();
       tc_fence_before();
-      if (i_row < p.nq) {
+      if (i_row < p.nq && !phantom_tile<kMcast>(p, tile)) {  // a phantom tile repeats its peer's
         __nv_bfloat16* dst;
         if constexpr (kPeerOut) {
           const int64_t nl = p.out_peers->n_local, rk = orow / nl;
@@ -720,12 +755,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // PV_{g-3} completed (in-order tcgen05 pipe, QK_{g+1} is issued after PV_{g-2}), so the
     // barrier is never more than one phase behind the one waited for.
     auto wait_pv = [&](uint32_t g) { mbar_wait(&bars->o_done[g % C::kSBufs], (g / C::kSBufs) & 1); };
-    TileMeta nxt = load_meta(p, blockIdx.x);
+    TileMeta nxt = load_meta(p, tile_at<kMcast>(p, 0));
     int32_t vb_first = nxt.cnt > 0 ? block_at(p, nxt.beg, 0) : 0;
-    for (int64_t tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+    for (int64_t it = 0, tile = tile_at<kMcast>(p, 0); tile >= 0; tile = tile_at<kMcast>(p, ++it)) {
       const int64_t h = tile / p.mq, u = tile % p.mq;
       const int32_t beg = nxt.beg, cnt = nxt.cnt;
-      nxt = load_meta(p, tile + gridDim.x);
+      nxt = load_meta(p, tile_at<kMcast>(p, it + 1));
       const int64_t i_row = u * kBM + r;  // this thread's query row, and its raster slot
       const int64_t orow = i_row < p.nq && p.out_rows ? int64_t(__ldg(p.out_rows + i_row)) : i_row;
       float m = -INFINITY;
@@ -954,6 +989,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (kMcast) cluster_sync();  // no CTA leaves while its peer may still signal or fill it
   if (warp == kMmaWarp) tmem_dealloc<kTmemCols>(tmem);
 }
 
@@ -1024,15 +1060,41 @@ int make_gather_map(CUtensorMap* map, const void* base, int64_t rows, int64_t d)
   return DFS_OK;
 }
 
+// dense steps (full key list): 2-CTA clusters with K/V tiles multicast into both CTAs
+#ifndef DFS_ATTN_MCAST
+#define DFS_ATTN_MCAST 1
+#endif
+
 template <int D, int POLY, bool kPeerOut = false>
 int launch_kernel(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const Params& p,
                   cudaStream_t stream) {
   using C = Cfg<D>;
+  if (DFS_ATTN_MCAST && !kPeerOut && !p.blk_ptr && kWG == 2 && DFS_ATTN_ROWSPLIT) {
+    auto* kfn = attn_sm100_kernel<D, POLY, kPeerOut, true>;
+    DFS_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    const int64_t pairs = p.heads * ((p.mq + 1) / 2);
+    const int64_t grid = 2 * (pairs < kNumSMs / 2 ? pairs : kNumSMs / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DFS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kfn, mq, mk, mv, p));
+    DFS_LAUNCH_CHECK("attn_sm100 (dense, multicast)");
+    return DFS_OK;
+  }
   // per device and race-free: set on every launch (~1 us)
-  DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D, POLY, kPeerOut>,
+  DFS_CUDA_CHECK(cudaFuncSetAttribute(attn_sm100_kernel<D, POLY, kPeerOut, false>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
   const int64_t grid = p.tiles < kNumSMs ? p.tiles : kNumSMs;
-  attn_sm100_kernel<D, POLY, kPeerOut><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
+  attn_sm100_kernel<D, POLY, kPeerOut, false><<<unsigned(grid), kThreads, C::kSmem, stream>>>(mq, mk, mv, p);
   DFS_LAUNCH_CHECK("attn_sm100");
   return DFS_OK;
 }
@@ -1081,6 +1143,15 @@ int launch(const dfs_attn_args& a, float scale, cudaStream_t stream) {
   if (p.trace) DFS_CUDA_CHECK(cudaMemsetAsync(p.trace, 0, 40 * 256 * sizeof(unsigned long long), stream));
 #endif
   static const int poly = getenv("DFS_ATTN_POLY") ? atoi(getenv("DFS_ATTN_POLY")) : kDefaultPoly<D>;
+  // a trajectory runs dense (multicast) and sparse steps: load both kernels on the first call,
+  // not inside the first step that needs the other one (lazy module loading costs ~ms)
+  static const bool loaded = [] {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, attn_sm100_kernel<D, kDefaultPoly<D>, false, false>);
+    cudaFuncGetAttributes(&fa, attn_sm100_kernel<D, kDefaultPoly<D>, false, true>);
+    return true;
+  }();
+  (void)loaded;
   if (a.out_peers) {  // Ulysses: the epilogue stores into the token owners' shards
     rc = launch_kernel<D, kDefaultPoly<D>, true>(mq, mk, mv, p, stream);
   } else {

@@ -131,6 +131,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// one box multicast into the same shared-memory offset of both CTAs of a 2-CTA cluster,
+// completion counted on each CTA's barrier at `bar`'s offset
+__device__ __forceinline__ void tma_load_3d_mcast2(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                   int c2) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1, {%3, %4, %5}], [%2], m;\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // pair load: this CTA's box into its own shared memory, completion counted on the
 // leader's barrier at the same offset
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, const uint64_t* bar, int c0,
@@ -348,6 +360,14 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// MMA completion -> the barrier at this offset in both CTAs of a 2-CTA cluster (cta_group::1)
+__device__ __forceinline__ void umma_commit_both(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
           smem_u32(bar))
       : "memory");
 }
