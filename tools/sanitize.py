@@ -1,7 +1,8 @@
 """Small launches of every hot-path kernel for compute-sanitizer (memcheck / racecheck /
 synccheck): python tools/sanitize.py. Config T (B = 64, tcgen05 union tiles), a B = 128,
 d = 128 and a d = 64 step (K2, K3 tcgen05 pairs, K4, K5), the fused-exchange Ulysses
-step over two simulated ranks, the fp32 compatibility step and the streamed recall."""
+step over two simulated ranks, the fp32 compatibility step, the streamed recall and dense
+(warmup) steps through the multicast cluster kernel."""
 import os
 import sys
 
@@ -27,7 +28,20 @@ def step(dims, h, d, b, dtype=torch.bfloat16, recall=False):
     return q, k, v
 
 
+def dense(dims, h, d):
+    """A dense (warmup) step: K5 over the full key list in 2-CTA clusters with multicast K/V."""
+    n = dims[0] * dims[1] * dims[2]
+    g = torch.Generator().manual_seed(n + 7 * d)
+    q, k, v = (torch.randn(n, h, d, generator=g).to(torch.bfloat16).cuda() for _ in range(3))
+    sched = dfs.SparsitySchedule(total_steps=4, warmup_fraction=0.5, phase_budgets=(0.25,), phase_fraction=0.5,
+                                 update_interval=1)  # steps 0 and 1 are dense
+    dfs.run_step(q, k, v, dims, dfs.ScoringParams(128, 16), sched, dfs.MaskCache(), layer=0, step=0)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
+    dense((4, 16, 32), 2, 128)  # 16 query blocks per head
+    dense((3, 16, 45), 3, 64)  # 17 per head: the odd CTA's phantom tile
     step((4, 8, 8), 2, 64, 64)
     step((4, 16, 32), 2, 128, 128, recall=True)
     step((3, 16, 45), 2, 64, 128)
