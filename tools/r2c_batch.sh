@@ -14,11 +14,5 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:'attn_sm100|score_sm100|permute_kernel|topk|absmax|split_kernel|lut_ptr' -s 12 -c 12 \
   -o $OUT/prof python tools/profile_step.py HY > $OUT/ncu.log 2>&1
-for tool in memcheck racecheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize.py > $OUT/sanitize_$tool.log 2>&1
-  echo "sanitize $tool rc=$?" >> $OUT/summary.txt
-done
-DFS_B200_LIB=build/ab/lib_sync.so timeout 900 compute-sanitizer --tool synccheck --print-limit 20 \
-  python tools/sanitize.py > $OUT/sanitize_synccheck.log 2>&1
-echo "sanitize synccheck rc=$?" >> $OUT/summary.txt
+# compute-sanitizer (tools/sanitize.sh) is closed on the GPU pool since r2m; run it separately where allowed
 echo done >> $OUT/summary.txt
